@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""bench.py — sketch-apply throughput (BASELINE.json metric) on 1..8 B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config ls] [--variant auto]
+    torchrun --nproc-per-node N bench.py --gpus N ...            (N > 1, one rank per GPU)
+    python bench.py --impl reference ...                          (the CPU oracle arm)
+
+A step is one bps_apply (the whole hot path: wiring, hashing, streaming, accumulation,
+epilogue — SURVEY §8a rows a1-a7) over the config's synthetic d×n input, resident in
+HBM.  Multi-GPU is weak scaling: every rank applies the same sketch to its own n-column
+batch (column sharding needs no collective); value = all ranks' bytes ÷
+the max-over-ranks device time.  Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sketch-apply GB/s and columns/s per GPU (% of HBM roofline) at 1/2/4/8 B200"
+UNIT = "GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="ls")
+    ap.add_argument("--variant", default="auto", choices=["auto", "sparse", "tc"])
+    ap.add_argument("--kind", default="gaussian", choices=["gaussian", "coherent", "lowrank"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(cfg_name, variant):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(cfg_name, {}).get(variant)
+
+
+class Clocks:
+    """Sample nvidia-smi clocks/throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str, enabled=True):
+        self.gpu_id, self.enabled, self.rows, self.proc = gpu_id, enabled, [], None
+
+    def start(self):
+        if not self.enabled:
+            return
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(1)
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(cfg, n_sample, repeats=2):
+    """Time the oracle as it stands on a bounded column sample (rank 0, N=1)."""
+    import numpy as np
+
+    import oracle
+    import synth
+
+    osk = oracle.make_sketch(cfg.M, cfg.B_r, cfg.B_c, cfg.kappa, cfg.s, cfg.seed)
+    A = synth.host_matrix("gaussian", cfg.d, n_sample, seed=3, dtype=np.float32)
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        oracle.apply(osk, A)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return t, cfg.roofline_bytes(n_sample)
+
+
+def reference_arm(args, cfg, rank):
+    if rank != 0:
+        return
+    import numpy as np
+
+    n_s = max(1, min(cfg.n, 32))
+    # each step = the oracle on a bounded n_s-column sample of the config
+    import oracle
+    import synth
+
+    osk = oracle.make_sketch(cfg.M, cfg.B_r, cfg.B_c, cfg.kappa, cfg.s, cfg.seed)
+    A = synth.host_matrix("gaussian", cfg.d, n_s, seed=3, dtype=np.float32)
+    for _ in range(args.warmup):
+        oracle.apply(osk, A)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.apply(osk, A)
+    dt = (time.perf_counter() - t0) / args.steps
+    gbs = cfg.roofline_bytes(n_s) / dt / 1e9
+    sample = f"{n_s} of {cfg.n} columns of the {cfg.name} config per step (S built + multiplied in float64)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic gaussian (host, numpy)",
+        "config": {"workload": cfg.name, "d": cfg.d, "k": cfg.k, "kappa": cfg.kappa, "s": cfg.s, "n": n_s,
+                   "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c},
+        "columns_per_s": n_s / dt,
+        "cpu_baseline": {"value": gbs, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": gbs, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2602_06071_b200 import configs as C
+
+    cfg = C.CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfg, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2602_06071_b200 import Sketch, lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = cfg.n
+    tdt = torch.float32 if cfg.dtype == "f32" else torch.bfloat16
+    sk = Sketch(**cfg.sketch_args())
+    A = synth.device_matrix(args.kind, cfg.d, n, seed=1000 + rank, M=cfg.M, dtype=tdt, device=dev)
+    Y = torch.empty((cfg.k, n), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        sk.apply(A, out=Y, variant=args.variant)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    uuid = str(torch.cuda.get_device_properties(dev).uuid)
+    clocks = Clocks(uuid if uuid.startswith("GPU-") else ("GPU-" + uuid), enabled=not args.no_clocks)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    l0 = lib.bps_kernel_launches()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record(stream)
+    for i in range(args.steps):
+        step()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    launches = lib.bps_kernel_launches() - l0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total = ev[0].elapsed_time(ev[-1])
+    t = torch.tensor([total], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_max = float(t.item())
+    ms = total_max / args.steps
+    bytes_rank = cfg.roofline_bytes(n)
+    value = world * bytes_rank / (ms / 1e3) / 1e9
+    peak, peak_src = measured_peaks()
+    achieved = bytes_rank / (statistics.mean(per) / 1e3) / 1e9
+
+    # end-to-end through the public API with pinned host buffers (H2D + apply + D2H per step)
+    e2e = None
+    if not args.no_e2e:
+        max_e2e_bytes = 8 << 30
+        n_e = n if bytes_rank <= max_e2e_bytes else max(128, int(n * max_e2e_bytes / bytes_rank) // 128 * 128)
+        A_h = torch.empty((cfg.d, n_e), dtype=tdt, pin_memory=True)
+        A_h.copy_(A[:, :n_e].cpu() if n_e < n else A.cpu())
+        Y_h = torch.empty((cfg.k, n_e), dtype=torch.float32, pin_memory=True)
+        A_d = A if n_e == n else torch.empty((cfg.d, n_e), dtype=tdt, device=dev)
+        Y_d = Y if n_e == n else torch.empty((cfg.k, n_e), dtype=torch.float32, device=dev)
+
+        def e2e_step():
+            A_d.copy_(A_h, non_blocking=True)
+            sk.apply(A_d, out=Y_d, variant=args.variant)
+            Y_h.copy_(Y_d, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        te = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = cfg.d * n_e * cfg.elem
+        d2h = cfg.k * n_e * 4
+        e2e = {"value": world * cfg.roofline_bytes(n_e) / (float(te.item()) / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "columns": n_e,
+               "ms_per_step": float(te.item())}
+        del A_h, Y_h
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_s = min(cfg.n, 64)
+        t_cpu, b_cpu = cpu_baseline(cfg, n_s)
+        cpu = {"value": b_cpu / t_cpu / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{n_s} of {cfg.n} columns of {cfg.name}, float64 S build + CSR multiply, median of 2 "
+                         f"({t_cpu:.2f} s each); numpy/scipy single-threaded",
+               "host_cores_available": len(os.sched_getaffinity(0))}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" else "bf16-in/f32-acc",
+            "data": f"synthetic {args.kind} (torch Philox on device), seed {1000}+rank",
+            "config": {"workload": cfg.name, "d": cfg.d, "k": cfg.k, "kappa": cfg.kappa, "s": cfg.s,
+                       "n_per_gpu": n, "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c, "variant": args.variant,
+                       "parallelism": f"column-shard x{world} (no collective)",
+                       "l2": "inputs larger than L2 (no flush needed)" if bytes_rank > (256 << 20) else "input fits L2"},
+            "columns_per_s": world * n / (ms / 1e3),
+            "gbs_per_gpu": value / world,
+            "frac_of_8tbs": value / world / 8000.0,
+            "ms_min": min(per), "ms_median": statistics.median(per),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": ncu_traffic(cfg.name, args.variant), "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": bytes_rank},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

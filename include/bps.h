@@ -1,0 +1,158 @@
+/*
+ * bps.h — C ABI of libbps: BlockPerm-SJLT sketch apply Y = S·A on NVIDIA B200 (sm_100a).
+ *
+ * The operation is the one defined in arXiv 2602.06071 ("FlashSketch"); citations
+ * "P:n" are lines of the paper text, "R<k>" the readings
+ * frozen in DESIGN.md §3 for what the paper leaves open.
+ *
+ *   d = M·B_c, k = M·B_r
+ *   N(g) = (f^1(g), ..., f^κ(g)),  f(x) = (a·x + b) mod M        ((a,b) by R4)
+ *   S_{g,h} = κ^{-1/2} Φ_{g,h} for h ∈ N(g), 0 otherwise
+ *   Φ_{g,h}: row-partitioned SJLT, s nonzeros ±1/√s per column   (R1-R3)
+ *   Y = S·A, each column of S has κ·s nonzeros of magnitude 1/√(κs)
+ *
+ * S is never stored: wiring, rows and signs are regenerated on the fly from a
+ * counter hash of (seed, g, ℓ, u, j) (R2).
+ *
+ * Conventions (all entry points):
+ *   - Return BPS_OK (0) on success or a negative bps_status; the message of the last
+ *     failure on the calling thread is available from bps_last_error().
+ *   - Validation happens before any device work; on a validation error no output is
+ *     touched.
+ *   - Device pointers are caller-owned CUDA device memory (e.g. torch tensors); the
+ *     library never allocates, frees or copies them and holds no device memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream); work
+ *     is enqueued asynchronously on it, with no implicit synchronisation. Execution
+ *     faults surface at the caller's next synchronisation.
+ *   - The current CUDA device is used and must be compute capability 10.0 (B200);
+ *     otherwise BPS_ERR_ARCH. There is no CPU fallback.
+ *   - Handles are immutable after creation; concurrent use from several threads or
+ *     streams is safe.
+ */
+#ifndef BPS_H_
+#define BPS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bps_sketch bps_sketch; /* opaque, host-only */
+
+typedef enum { BPS_F32 = 0, BPS_BF16 = 1 } bps_dtype;
+
+typedef enum {
+  BPS_OK = 0,
+  BPS_ERR_INVALID_ARG = -1, /* bad size / pointer / parameter */
+  BPS_ERR_ALIGNMENT = -2,   /* pointer or leading dimension not 16-byte aligned */
+  BPS_ERR_UNSUPPORTED = -3, /* valid sketch, but no kernel variant for this shape / variant request */
+  BPS_ERR_ARCH = -4,        /* current device is not sm_100 */
+  BPS_ERR_CUDA = -5,        /* a CUDA runtime / driver call failed (message has the CUDA error string) */
+  BPS_ERR_OVERFLOW = -6     /* a size product does not fit the supported integer range */
+} bps_status;
+
+/* Kernel variant selector for bps_apply_ex / bps_apply_t_ex. */
+typedef enum {
+  BPS_VARIANT_AUTO = 0,   /* tcgen05 path when supported for the shape, else the sparse path */
+  BPS_VARIANT_SPARSE = 1, /* CUDA-core gather kernel (private smem accumulators, no atomics) */
+  BPS_VARIANT_TC = 2      /* tcgen05 tensor-core kernel; BPS_ERR_UNSUPPORTED if the shape is not covered */
+} bps_variant;
+
+/*
+ * bps_make_sketch — create the sketch S for layout (M, B_r, B_c) and parameters (κ, s, seed).
+ *   d = M·B_c rows of A consumed, k = M·B_r rows of Y produced.
+ *   Requirements (SPEC S:40-41 restating P:1531; counter widths R2):
+ *     1 ≤ M < 2^24, 1 ≤ B_r, 1 ≤ B_c < 2^24, 1 ≤ κ ≤ min(M, 256),
+ *     1 ≤ s ≤ min(B_r, 256), B_r % s == 0, M·B_c and M·B_r < 2^62.
+ *   (a, b) are derived from the seed by R4 (Hull–Dobell).
+ *   Host-only; no device work. *out receives a handle freed by bps_free_sketch.
+ *   Errors: BPS_ERR_INVALID_ARG (out==NULL or a requirement violated), BPS_ERR_OVERFLOW.
+ */
+int bps_make_sketch(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t s,
+                    uint64_t seed, bps_sketch** out);
+
+/* bps_free_sketch — release a handle. NULL-safe. */
+void bps_free_sketch(bps_sketch* sk);
+
+/*
+ * bps_sketch_info — read back derived quantities. Any out-pointer may be NULL.
+ *   d, k: dimensions; a, b: wiring map f(x)=(a x+b) mod M; scale: fp32(1/√(κs)) (R6).
+ */
+int bps_sketch_info(const bps_sketch* sk, int64_t* d, int64_t* k, uint32_t* a, uint32_t* b,
+                    float* scale);
+
+/*
+ * bps_apply — Y = S·A  (output tile Y[gB_r:(g+1)B_r, columns]).
+ *   A : device, d×n row-major, element type `dtype`, leading dimension lda ≥ n (elements).
+ *   Y : device, k×n row-major fp32, leading dimension ldy ≥ n (elements). Overwritten.
+ *   bf16 inputs are widened exactly; accumulation is fp32; the scale 1/√(κs) is
+ *   applied once at the end as an fp32 constant (R6).
+ *   n == 0 is a no-op. A and Y must not overlap.
+ *   Alignment: A, Y 16-byte aligned and lda·elem, ldy·4 multiples of 16 bytes,
+ *   otherwise BPS_ERR_ALIGNMENT.
+ *   Determinism: for a fixed handle, input, n, dtype and variant, Y is bitwise
+ *   reproducible run to run.
+ */
+int bps_apply(const bps_sketch* sk, const void* A, int64_t lda, int64_t n, bps_dtype dtype,
+              float* Y, int64_t ldy, void* stream);
+
+/*
+ * bps_apply_t — transposed layout (R8): X = Aᵀ given n×d row-major (one length-d vector
+ *   per row, ldx ≥ d), output Yt = (S·Xᵀ)ᵀ, n×k row-major fp32 (ldyt ≥ k).
+ *   Same dtype, alignment, determinism and error rules as bps_apply.
+ */
+int bps_apply_t(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, bps_dtype dtype,
+                float* Yt, int64_t ldyt, void* stream);
+
+/* Explicit-variant forms (tests / benchmarking). BPS_ERR_UNSUPPORTED if the requested
+ * variant does not cover the shape. */
+int bps_apply_ex(const bps_sketch* sk, const void* A, int64_t lda, int64_t n, bps_dtype dtype,
+                 float* Y, int64_t ldy, void* stream, int variant);
+int bps_apply_t_ex(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, bps_dtype dtype,
+                   float* Yt, int64_t ldyt, void* stream, int variant);
+
+/*
+ * bps_orbit — the wiring orbit g_pos = f^pos(0), pos = 0..M-1 (host).
+ *   With this ordering N(g_i) = (g_{i+1}, ..., g_{i+κ}) (indices mod M), which is what
+ *   makes block sharding contiguous.  g_of_pos: host array of length M.
+ */
+int bps_orbit(const bps_sketch* sk, int32_t* g_of_pos);
+
+/*
+ * bps_apply_orbit_range — partial apply over orbit positions [pos_begin, pos_end)
+ *   (0 ≤ pos_begin < M, pos_begin < pos_end ≤ pos_begin + M; positions taken mod M).
+ *   A_local: device, the input blocks at orbit positions pos_begin+1 .. pos_end+κ-1,
+ *            stacked in that order: ((pos_end-pos_begin)+κ-1)·B_c rows × n, row-major, lda.
+ *   Y_local: device, the output blocks at orbit positions pos_begin .. pos_end-1,
+ *            stacked: (pos_end-pos_begin)·B_r rows × n fp32, row-major, ldy.
+ *   Output block at local index i equals rows g_{pos_begin+i}·B_r.. of the full S·A.
+ */
+int bps_apply_orbit_range(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end,
+                          const void* A_local, int64_t lda, int64_t n, bps_dtype dtype,
+                          float* Y_local, int64_t ldy, void* stream, int variant);
+
+/*
+ * bps_pattern_host — host evaluation of the frozen pattern draw (R2-R3), for tests:
+ *   row ∈ [0, B_r) inside output block g and sign ∈ {+1,-1} of the j-th nonzero of
+ *   column u of Φ_{g, f^ℓ(g)} (ell is 1-based). Uses the same code as the device kernels.
+ */
+int bps_pattern_host(const bps_sketch* sk, int64_t g, int32_t ell, int64_t u, int32_t j,
+                     int32_t* row, int32_t* sign);
+
+/* Number of CUDA kernels libbps has launched in this process so far (all devices, all
+ * threads; cudaMemsetAsync nodes are not counted). Used by the bench to report how
+ * many of the library's own kernels ran inside a timed region. */
+uint64_t bps_kernel_launches(void);
+
+/* Library / build information ("bps <version> sm_100a ..."). */
+const char* bps_version(void);
+
+/* Thread-local message describing the last failure on this thread ("" if none). */
+const char* bps_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BPS_H_ */

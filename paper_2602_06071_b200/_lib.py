@@ -1,0 +1,75 @@
+"""ctypes loader for libbps.so (C ABI declared in include/bps.h)."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libbps.so")
+
+BPS_OK = 0
+STATUS = {
+    0: "BPS_OK",
+    -1: "BPS_ERR_INVALID_ARG",
+    -2: "BPS_ERR_ALIGNMENT",
+    -3: "BPS_ERR_UNSUPPORTED",
+    -4: "BPS_ERR_ARCH",
+    -5: "BPS_ERR_CUDA",
+    -6: "BPS_ERR_OVERFLOW",
+}
+EXPORTS = [
+    "bps_make_sketch", "bps_free_sketch", "bps_sketch_info", "bps_apply", "bps_apply_t", "bps_apply_ex",
+    "bps_apply_t_ex", "bps_orbit", "bps_apply_orbit_range", "bps_pattern_host", "bps_kernel_launches", "bps_version", "bps_last_error",
+]
+
+
+class BpsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(lib_path):
+        raise ImportError(
+            f"libbps.so not found at {lib_path}; build it with `python -m paper_2602_06071_b200.build` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(lib_path)
+    i64, i32, u64, u32, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p
+    L.bps_make_sketch.argtypes = [i64, i64, i64, i32, i32, u64, ctypes.POINTER(vp)]
+    L.bps_make_sketch.restype = ctypes.c_int
+    L.bps_free_sketch.argtypes = [vp]
+    L.bps_free_sketch.restype = None
+    L.bps_sketch_info.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(u32),
+                                  ctypes.POINTER(u32), ctypes.POINTER(ctypes.c_float)]
+    L.bps_sketch_info.restype = ctypes.c_int
+    for name in ("bps_apply", "bps_apply_t"):
+        f = getattr(L, name)
+        f.argtypes = [vp, vp, i64, i64, ctypes.c_int, vp, i64, vp]
+        f.restype = ctypes.c_int
+    for name in ("bps_apply_ex", "bps_apply_t_ex"):
+        f = getattr(L, name)
+        f.argtypes = [vp, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_int]
+        f.restype = ctypes.c_int
+    L.bps_orbit.argtypes = [vp, ctypes.POINTER(i32)]
+    L.bps_orbit.restype = ctypes.c_int
+    L.bps_apply_orbit_range.argtypes = [vp, i64, i64, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_int]
+    L.bps_apply_orbit_range.restype = ctypes.c_int
+    L.bps_pattern_host.argtypes = [vp, i64, i32, i64, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    L.bps_pattern_host.restype = ctypes.c_int
+    L.bps_kernel_launches.argtypes = []
+    L.bps_kernel_launches.restype = ctypes.c_uint64
+    L.bps_version.argtypes = []
+    L.bps_version.restype = ctypes.c_char_p
+    L.bps_last_error.argtypes = []
+    L.bps_last_error.restype = ctypes.c_char_p
+    return L
+
+
+lib = _load()
+
+
+def check(rc: int) -> None:
+    if rc != BPS_OK:
+        raise BpsError(rc, lib.bps_last_error().decode(errors="replace"))

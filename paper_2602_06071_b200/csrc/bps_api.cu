@@ -1,0 +1,244 @@
+// bps_api.cu — the C ABI of libbps (include/bps.h): handle creation, validation and
+// kernel dispatch.  All hot work happens in bps_sparse.cu / bps_tc.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <numeric>
+#include <string>
+
+#include "bps_internal.h"
+
+namespace bps {
+
+static thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+static uint64_t rad(uint64_t M) {
+  uint64_t r = 1, m = M;
+  for (uint64_t q = 2; q * q <= m; ++q) {
+    if (m % q == 0) {
+      r *= q;
+      while (m % q == 0) m /= q;
+    }
+  }
+  if (m > 1) r *= m;
+  return r;
+}
+
+// R4: (a, b) from the seed, Hull–Dobell full period.
+static void select_affine(uint64_t seed, uint64_t M, uint32_t* a, uint32_t* b) {
+  if (M == 1) {
+    *a = 0;
+    *b = 0;
+    return;
+  }
+  uint64_t q = rad(M);
+  if (M % 4 == 0) q *= 2;
+  *a = (uint32_t)((1 + q * (mix64(seed ^ kTagA) % (M / q))) % M);
+  for (uint64_t t = 0;; ++t) {
+    uint64_t bb = mix64(seed ^ kTagB ^ t) % M;
+    if (std::gcd(bb, M) == 1) {
+      *b = (uint32_t)bb;
+      return;
+    }
+  }
+}
+
+// Device check: cc 10.0 required (BJ: no multi-backend dispatch).
+static int check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+  static std::mutex mu;
+  static int cached[64];
+  static bool init = false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!init) {
+    for (int& c : cached) c = -1;
+    init = true;
+  }
+  if (dev < 0 || dev >= 64) return fail(BPS_ERR_CUDA, "device ordinal out of range");
+  if (cached[dev] < 0) {
+    int maj = 0, min = 0;
+    if (cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+      return fail(BPS_ERR_CUDA, "cudaDeviceGetAttribute failed");
+    cached[dev] = maj * 10 + min;
+  }
+  if (cached[dev] != 100)
+    return fail(BPS_ERR_ARCH, "libbps is built for sm_100a (B200); current device has cc " +
+                                  std::to_string(cached[dev] / 10) + "." + std::to_string(cached[dev] % 10));
+  return BPS_OK;
+}
+
+static int elem_size(bps_dtype dt) { return dt == BPS_F32 ? 4 : (dt == BPS_BF16 ? 2 : 0); }
+
+static bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return x < y + nb && y < x + na;
+}
+
+// Common validation for the three apply entry points.
+static int validate_apply(const bps_sketch* sk, const void* in, int64_t ldin, int64_t in_rows, int64_t in_cols,
+                          bps_dtype dt, const float* out, int64_t ldout, int64_t out_rows, int64_t out_cols,
+                          int variant) {
+  if (!sk) return fail(BPS_ERR_INVALID_ARG, "sketch handle is NULL");
+  const int es = elem_size(dt);
+  if (!es) return fail(BPS_ERR_INVALID_ARG, "dtype must be BPS_F32 or BPS_BF16");
+  if (variant < BPS_VARIANT_AUTO || variant > BPS_VARIANT_TC) return fail(BPS_ERR_INVALID_ARG, "unknown variant");
+  if (in_rows < 0 || in_cols < 0 || out_rows < 0 || out_cols < 0) return fail(BPS_ERR_INVALID_ARG, "negative size");
+  if (in_rows == 0 || in_cols == 0 || out_rows == 0 || out_cols == 0) return BPS_OK;  // n == 0: no-op
+  if (!in || !out) return fail(BPS_ERR_INVALID_ARG, "NULL data pointer");
+  if (ldin < in_cols) return fail(BPS_ERR_INVALID_ARG, "input leading dimension smaller than its row length");
+  if (ldout < out_cols) return fail(BPS_ERR_INVALID_ARG, "output leading dimension smaller than its row length");
+  if (ldin > (int64_t(1) << 40) || ldout > (int64_t(1) << 40)) return fail(BPS_ERR_OVERFLOW, "leading dimension too large");
+  if (((uintptr_t)in % 16) || ((uintptr_t)out % 16) || ((ldin * es) % 16) || ((ldout * 4) % 16))
+    return fail(BPS_ERR_ALIGNMENT, "pointers and leading dimensions must be 16-byte aligned");
+  const size_t in_bytes = (size_t)((in_rows - 1) * ldin + in_cols) * es;
+  const size_t out_bytes = (size_t)((out_rows - 1) * ldout + out_cols) * 4;
+  if (overlaps(in, in_bytes, out, out_bytes)) return fail(BPS_ERR_INVALID_ARG, "input and output overlap");
+  return BPS_OK;
+}
+
+static int dispatch(const bps_sketch* sk, const void* in, int64_t ldin, int64_t n, bps_dtype dt, float* out,
+                    int64_t ldout, bool transposed, const Placement& pl, void* stream, int variant) {
+  int rc = check_device();
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool tc_ok = tc_supported(sk->p, n, dt, transposed, pl) == BPS_OK;
+  if (variant == BPS_VARIANT_TC && !tc_ok) return BPS_ERR_UNSUPPORTED;  // message set by tc_supported
+  if (tc_ok && variant != BPS_VARIANT_SPARSE) return launch_tc(sk->p, in, ldin, n, dt, out, ldout, transposed, pl, st);
+  return transposed ? launch_sparse_transposed(sk->p, in, ldin, n, dt, out, ldout, pl, st)
+                    : launch_sparse_rowmajor(sk->p, in, ldin, n, dt, out, ldout, pl, st);
+}
+
+}  // namespace bps
+
+using namespace bps;
+
+extern "C" {
+
+const char* bps_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t bps_kernel_launches(void) { return g_launches.load(); }
+
+const char* bps_version(void) { return "bps 0.1 sm_100a (sparse gather + tcgen05 NT band kernel)"; }
+
+int bps_make_sketch(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t s, uint64_t seed, bps_sketch** out) {
+  if (!out) return fail(BPS_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (M < 1 || B_r < 1 || B_c < 1) return fail(BPS_ERR_INVALID_ARG, "M, B_r, B_c must be >= 1");
+  if (M >= (int64_t(1) << 24)) return fail(BPS_ERR_INVALID_ARG, "M must be < 2^24 (counter field, R2)");
+  if (B_c >= (int64_t(1) << 24)) return fail(BPS_ERR_INVALID_ARG, "B_c must be < 2^24 (counter field, R2)");
+  if (B_r >= (int64_t(1) << 31)) return fail(BPS_ERR_INVALID_ARG, "B_r too large");
+  if (kappa < 1 || kappa > M || kappa > 256) return fail(BPS_ERR_INVALID_ARG, "need 1 <= kappa <= min(M, 256) (P:1531)");
+  if (s < 1 || s > B_r || s > 256 || B_r % s != 0)
+    return fail(BPS_ERR_INVALID_ARG, "need 1 <= s <= min(B_r, 256) and B_r % s == 0 (row-partitioned, R1)");
+  if (M > (int64_t(1) << 62) / B_c || M > (int64_t(1) << 62) / B_r) return fail(BPS_ERR_OVERFLOW, "M*B_c or M*B_r overflows");
+  bps_sketch* sk = new (std::nothrow) bps_sketch;
+  if (!sk) return fail(BPS_ERR_INVALID_ARG, "out of host memory");
+  sk->M = M;
+  sk->B_r = B_r;
+  sk->B_c = B_c;
+  sk->d = M * B_c;
+  sk->k = M * B_r;
+  sk->kappa = kappa;
+  sk->s = s;
+  sk->seed = seed;
+  SketchParams& p = sk->p;
+  p.M = (uint32_t)M;
+  p.B_r = (uint32_t)B_r;
+  p.B_c = (uint32_t)B_c;
+  p.kappa = (uint32_t)kappa;
+  p.s = (uint32_t)s;
+  p.C = (uint32_t)(B_r / s);
+  select_affine(seed, (uint64_t)M, &p.a, &p.b);
+  p.K = mix64(seed ^ kTagPhi);
+  p.scale = (float)(1.0 / std::sqrt((double)kappa * (double)s));
+  *out = sk;
+  return BPS_OK;
+}
+
+void bps_free_sketch(bps_sketch* sk) { delete sk; }
+
+int bps_sketch_info(const bps_sketch* sk, int64_t* d, int64_t* k, uint32_t* a, uint32_t* b, float* scale) {
+  if (!sk) return fail(BPS_ERR_INVALID_ARG, "sketch handle is NULL");
+  if (d) *d = sk->d;
+  if (k) *k = sk->k;
+  if (a) *a = sk->p.a;
+  if (b) *b = sk->p.b;
+  if (scale) *scale = sk->p.scale;
+  return BPS_OK;
+}
+
+int bps_orbit(const bps_sketch* sk, int32_t* g_of_pos) {
+  if (!sk || !g_of_pos) return fail(BPS_ERR_INVALID_ARG, "NULL argument");
+  uint32_t x = 0;
+  for (int64_t i = 0; i < sk->M; ++i) {
+    g_of_pos[i] = (int32_t)x;
+    x = affine_step(sk->p, x);
+  }
+  return BPS_OK;
+}
+
+int bps_pattern_host(const bps_sketch* sk, int64_t g, int32_t ell, int64_t u, int32_t j, int32_t* row, int32_t* sign) {
+  if (!sk || !row || !sign) return fail(BPS_ERR_INVALID_ARG, "NULL argument");
+  if (g < 0 || g >= sk->M || ell < 1 || ell > sk->kappa || u < 0 || u >= sk->B_c || j < 0 || j >= sk->s)
+    return fail(BPS_ERR_INVALID_ARG, "index out of range");
+  Draw dr = pattern(sk->p, (uint32_t)g, (uint32_t)ell, (uint32_t)u, (uint32_t)j);
+  *row = (int32_t)dr.row;
+  *sign = dr.neg ? -1 : 1;
+  return BPS_OK;
+}
+
+int bps_apply_ex(const bps_sketch* sk, const void* A, int64_t lda, int64_t n, bps_dtype dtype, float* Y, int64_t ldy,
+                 void* stream, int variant) {
+  int rc = validate_apply(sk, A, lda, sk ? sk->d : 0, n, dtype, Y, ldy, sk ? sk->k : 0, n, variant);
+  if (rc || n == 0) return rc;
+  Placement pl{0, 0, sk->M};
+  return dispatch(sk, A, lda, n, dtype, Y, ldy, false, pl, stream, variant);
+}
+
+int bps_apply(const bps_sketch* sk, const void* A, int64_t lda, int64_t n, bps_dtype dtype, float* Y, int64_t ldy,
+              void* stream) {
+  return bps_apply_ex(sk, A, lda, n, dtype, Y, ldy, stream, BPS_VARIANT_AUTO);
+}
+
+int bps_apply_t_ex(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, bps_dtype dtype, float* Yt,
+                   int64_t ldyt, void* stream, int variant) {
+  int rc = validate_apply(sk, X, ldx, n, sk ? sk->d : 0, dtype, Yt, ldyt, n, sk ? sk->k : 0, variant);
+  if (rc || n == 0) return rc;
+  Placement pl{0, 0, sk->M};
+  return dispatch(sk, X, ldx, n, dtype, Yt, ldyt, true, pl, stream, variant);
+}
+
+int bps_apply_t(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, bps_dtype dtype, float* Yt, int64_t ldyt,
+                void* stream) {
+  return bps_apply_t_ex(sk, X, ldx, n, dtype, Yt, ldyt, stream, BPS_VARIANT_AUTO);
+}
+
+int bps_apply_orbit_range(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end, const void* A_local, int64_t lda,
+                          int64_t n, bps_dtype dtype, float* Y_local, int64_t ldy, void* stream, int variant) {
+  if (!sk) return fail(BPS_ERR_INVALID_ARG, "sketch handle is NULL");
+  if (pos_begin < 0 || pos_begin >= sk->M || pos_end <= pos_begin || pos_end > pos_begin + sk->M)
+    return fail(BPS_ERR_INVALID_ARG, "need 0 <= pos_begin < M and pos_begin < pos_end <= pos_begin + M");
+  const int64_t L = pos_end - pos_begin;
+  const int64_t in_rows = (L + sk->kappa - 1) * sk->B_c;
+  int rc = validate_apply(sk, A_local, lda, in_rows, n, dtype, Y_local, ldy, L * sk->B_r, n, variant);
+  if (rc || n == 0) return rc;
+  Placement pl{1, pos_begin, L};
+  return dispatch(sk, A_local, lda, n, dtype, Y_local, ldy, false, pl, stream, variant);
+}
+
+}  // extern "C"

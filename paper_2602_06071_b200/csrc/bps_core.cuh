@@ -1,0 +1,81 @@
+// bps_core.cuh — the frozen BlockPerm-SJLT randomness, shared by host code and every
+// device kernel of libbps (never by the oracle).  DESIGN.md §3 R1-R4.
+#pragma once
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define BPS_HD __host__ __device__ __forceinline__
+#else
+#define BPS_HD inline
+#endif
+
+namespace bps {
+
+constexpr uint64_t kTagA = 0xA11CE5EEDA11CE5EULL;
+constexpr uint64_t kTagB = 0xB0B5EEDB0B5EEDB0ULL;
+constexpr uint64_t kTagPhi = 0x5048495F5048495FULL;
+
+// MurmurHash3 fmix64 (R2; "fast mixing hash").
+BPS_HD uint64_t mix64(uint64_t z) {
+  z ^= z >> 33;
+  z *= 0xFF51AFD7ED558CCDULL;
+  z ^= z >> 33;
+  z *= 0xC4CEB9FE1A85EC53ULL;
+  z ^= z >> 33;
+  return z;
+}
+
+// Parameters every kernel needs; passed by value (fits in the param space).
+struct SketchParams {
+  uint32_t M, B_r, B_c, kappa, s, C;  // C = B_r / s (row-partition chunk, R1)
+  uint32_t a, b;                      // f(x) = (a x + b) mod M   (R4)
+  uint64_t K;                         // mix64(seed ^ kTagPhi)     (R2)
+  float scale;                        // fp32(1/sqrt(kappa*s))     (R6)
+};
+
+// f(x) = (a x + b) mod M.
+BPS_HD uint32_t affine_step(const SketchParams& p, uint32_t x) {
+  return (uint32_t)(((uint64_t)p.a * x + p.b) % p.M);
+}
+
+// f^e(x) by composing affine maps (square-and-multiply), e ≥ 0.
+BPS_HD uint32_t affine_pow(const SketchParams& p, uint64_t e, uint32_t x) {
+  // Represent a map as (ma, mb): x -> ma x + mb (mod M).
+  uint64_t ra = 1 % p.M, rb = 0;           // accumulated result
+  uint64_t ba = p.a % p.M, bb = p.b % p.M; // f^(2^i)
+  const uint64_t M = p.M;
+  while (e) {
+    if (e & 1) {  // result = base ∘ result
+      rb = (ba * rb + bb) % M;
+      ra = (ba * ra) % M;
+    }
+    bb = (ba * bb + bb) % M;
+    ba = (ba * ba) % M;
+    e >>= 1;
+  }
+  return (uint32_t)((ra * x + rb) % M);
+}
+
+// Row (inside the output block) and sign of the j-th nonzero of column u of
+// Φ_{g, f^ell(g)}, ell 1-based (R1-R3; P:25-26 row-partitioned, P:1700 hash per (g,h,u,i)).
+struct Draw {
+  uint32_t row;
+  uint32_t neg;  // 1 => sign -1
+};
+
+BPS_HD uint64_t pattern_hash(const SketchParams& p, uint32_t g, uint32_t ell, uint32_t u, uint32_t j) {
+  const uint64_t ctr = ((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | ((uint64_t)u << 8) | (uint64_t)j;
+  return mix64(ctr ^ p.K);
+}
+
+BPS_HD Draw draw_from_hash(const SketchParams& p, uint64_t z, uint32_t j) {
+  const uint32_t hi = (uint32_t)(z >> 32);
+  const uint32_t off = (uint32_t)(((uint64_t)hi * p.C) >> 32);  // Lemire range on the high word (R3)
+  return Draw{j * p.C + off, (uint32_t)(z & 1)};
+}
+
+BPS_HD Draw pattern(const SketchParams& p, uint32_t g, uint32_t ell, uint32_t u, uint32_t j) {
+  return draw_from_hash(p, pattern_hash(p, g, ell, u, j), j);
+}
+
+}  // namespace bps

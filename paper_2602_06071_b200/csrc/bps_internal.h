@@ -1,0 +1,46 @@
+// bps_internal.h — declarations shared by the libbps translation units (not installed).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+#include "../../include/bps.h"
+#include "bps_core.cuh"
+
+struct bps_sketch {
+  bps::SketchParams p;
+  int64_t M, B_r, B_c, d, k;
+  int32_t kappa, s;
+  uint64_t seed;
+};
+
+namespace bps {
+
+extern std::atomic<uint64_t> g_launches;
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+// Where the CTA for output index o (grid.x) finds its data:
+//   full mode : o = g;  input block for ℓ at row f^ℓ(g)·B_c;  output rows g·B_r.
+//   range mode: o = local orbit index; g = f^(pos_begin+o)(0); input block for ℓ at local
+//               stacked block o+ℓ-1; output rows o·B_r.
+struct Placement {
+  int range_mode;
+  int64_t pos_begin;
+  int64_t n_out;  // number of output blocks launched (grid.x)
+};
+
+// Sparse CUDA-core kernels (bps_sparse.cu).
+int launch_sparse_rowmajor(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt,
+                           float* Y, int64_t ldy, const Placement& pl, cudaStream_t st);
+int launch_sparse_transposed(const SketchParams& p, const void* X, int64_t ldx, int64_t n, bps_dtype dt,
+                             float* Yt, int64_t ldyt, const Placement& pl, cudaStream_t st);
+
+// tcgen05 kernels (bps_tc.cu). Return BPS_ERR_UNSUPPORTED when the shape is not covered.
+int tc_supported(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl);
+int launch_tc(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt, float* Y, int64_t ldy,
+              bool transposed, const Placement& pl, cudaStream_t st);
+
+}  // namespace bps

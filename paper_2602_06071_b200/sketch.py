@@ -1,0 +1,130 @@
+"""`Sketch`: torch-tensor front end of the C ABI (argument marshalling only)."""
+
+from __future__ import annotations
+
+import ctypes
+
+from ._lib import check, lib
+
+BPS_F32, BPS_BF16 = 0, 1
+VARIANTS = {"auto": 0, "sparse": 1, "tc": 2}
+
+
+def _dtype_code(t) -> int:
+    import torch
+
+    if t.dtype == torch.float32:
+        return BPS_F32
+    if t.dtype == torch.bfloat16:
+        return BPS_BF16
+    raise TypeError(f"unsupported dtype {t.dtype} (float32 or bfloat16)")
+
+
+def _stream_ptr(device) -> int:
+    import torch
+
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _check_matrix(t, name):
+    if t.dim() != 2:
+        raise ValueError(f"{name} must be 2-D")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (libbps has no CPU path)")
+    if t.stride(1) != 1:
+        raise ValueError(f"{name} must be row-major with unit column stride")
+
+
+class Sketch:
+    """BlockPerm-SJLT S (k×d, k = M·B_r, d = M·B_c) regenerated on the fly (bps_make_sketch)."""
+
+    def __init__(self, M: int, B_r: int, B_c: int, kappa: int, s: int, seed: int = 0):
+        h = ctypes.c_void_p()
+        check(lib.bps_make_sketch(M, B_r, B_c, kappa, s, ctypes.c_uint64(seed & (2**64 - 1)), ctypes.byref(h)))
+        self._h = h
+        self.M, self.B_r, self.B_c, self.kappa, self.s, self.seed = M, B_r, B_c, kappa, s, seed & (2**64 - 1)
+        d, k = ctypes.c_int64(), ctypes.c_int64()
+        a, b = ctypes.c_uint32(), ctypes.c_uint32()
+        sc = ctypes.c_float()
+        check(lib.bps_sketch_info(h, ctypes.byref(d), ctypes.byref(k), ctypes.byref(a), ctypes.byref(b), ctypes.byref(sc)))
+        self.d, self.k, self.a, self.b, self.scale = d.value, k.value, a.value, b.value, sc.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.bps_free_sketch(h)
+            self._h = None
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    def info(self) -> dict:
+        return dict(M=self.M, B_r=self.B_r, B_c=self.B_c, kappa=self.kappa, s=self.s, seed=self.seed,
+                    d=self.d, k=self.k, a=self.a, b=self.b, scale=self.scale)
+
+    def orbit(self) -> list[int]:
+        arr = (ctypes.c_int32 * self.M)()
+        check(lib.bps_orbit(self._h, arr))
+        return list(arr)
+
+    def pattern(self, g: int, ell: int, u: int, j: int) -> tuple[int, int]:
+        r, sg = ctypes.c_int32(), ctypes.c_int32()
+        check(lib.bps_pattern_host(self._h, g, ell, u, j, ctypes.byref(r), ctypes.byref(sg)))
+        return r.value, sg.value
+
+    # ------------------------------------------------------------------ apply
+    def apply(self, A, out=None, variant: str = "auto"):
+        """Y = S·A. A: cuda d×n (float32/bfloat16, row-major, lda = A.stride(0)) -> k×n float32."""
+        import torch
+
+        _check_matrix(A, "A")
+        if A.shape[0] != self.d:
+            raise ValueError(f"A has {A.shape[0]} rows, sketch expects d={self.d}")
+        n = A.shape[1]
+        if out is None:
+            out = torch.empty((self.k, n), dtype=torch.float32, device=A.device)
+        _check_matrix(out, "out")
+        if out.dtype != torch.float32 or tuple(out.shape) != (self.k, n):
+            raise ValueError("out must be float32 k×n")
+        check(lib.bps_apply_ex(self._h, A.data_ptr(), A.stride(0), n, _dtype_code(A), out.data_ptr(), out.stride(0),
+                               _stream_ptr(A.device), VARIANTS[variant]))
+        return out
+
+    def apply_t(self, X, out=None, variant: str = "auto"):
+        """Transposed layout: X cuda n×d -> (S·Xᵀ)ᵀ, n×k float32."""
+        import torch
+
+        _check_matrix(X, "X")
+        if X.shape[1] != self.d:
+            raise ValueError(f"X has {X.shape[1]} columns, sketch expects d={self.d}")
+        n = X.shape[0]
+        if out is None:
+            out = torch.empty((n, self.k), dtype=torch.float32, device=X.device)
+        _check_matrix(out, "out")
+        if out.dtype != torch.float32 or tuple(out.shape) != (n, self.k):
+            raise ValueError("out must be float32 n×k")
+        check(lib.bps_apply_t_ex(self._h, X.data_ptr(), X.stride(0), n, _dtype_code(X), out.data_ptr(), out.stride(0),
+                                 _stream_ptr(X.device), VARIANTS[variant]))
+        return out
+
+    def apply_orbit_range(self, pos_begin: int, pos_end: int, A_local, out=None, variant: str = "auto"):
+        """Partial apply over orbit positions [pos_begin, pos_end) (bps_apply_orbit_range)."""
+        import torch
+
+        _check_matrix(A_local, "A_local")
+        L = pos_end - pos_begin
+        if A_local.shape[0] != (L + self.kappa - 1) * self.B_c:
+            raise ValueError("A_local must hold (L+kappa-1)*B_c rows")
+        n = A_local.shape[1]
+        if out is None:
+            out = torch.empty((L * self.B_r, n), dtype=torch.float32, device=A_local.device)
+        check(lib.bps_apply_orbit_range(self._h, pos_begin, pos_end, A_local.data_ptr(), A_local.stride(0), n,
+                                        _dtype_code(A_local), out.data_ptr(), out.stride(0),
+                                        _stream_ptr(A_local.device), VARIANTS[variant]))
+        return out
+
+    def apply_raw(self, A_ptr: int, lda: int, n: int, dtype_code: int, Y_ptr: int, ldy: int, stream: int,
+                  variant: str = "auto") -> None:
+        """Pointer-level call (used by the bench's CUDA-graph capture)."""
+        check(lib.bps_apply_ex(self._h, A_ptr, lda, n, dtype_code, Y_ptr, ldy, stream, VARIANTS[variant]))
