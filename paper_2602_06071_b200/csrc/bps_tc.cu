@@ -1,11 +1,553 @@
-// bps_tc.cu — tcgen05 tensor-core kernel (placeholder until the kernel lands).
+// bps_tc.cu — tcgen05 tensor-core kernel for Y = S·A (the "tc" variant). DESIGN.md §6.
+//
+// Idea: the block sparsity of S is a union of κ permutations that are powers of one
+// affine map f.  Ordering input and output blocks along the orbit
+// g_i = f^i(0) turns the wiring into a sliding window: output i reads input positions
+// i+1..i+κ.  A CTA streams a contiguous range of input positions once (no κ-fold
+// re-read), and for each input block p it builds the dense ±1
+// "band" B_p = [Φ_{g_{p-1},g_p}; …; Φ_{g_{p-κ},g_p}] (κ·B_r × B_c, bf16 exact, rows
+// rotated so output i always lands in slot i mod κ) from the counter hash (R2) and
+// feeds it to tcgen05.mma as the K-major A operand; the data tile (TMA, SW128) is
+// the B operand (MN-major for row-major A, K-major for the transposed layout).
+// D (TMEM, fp32) rows = band rows, columns = data columns; the κ slots accumulate
+// across input blocks, and after block p the slot of output p−κ is complete: the
+// epilogue warps drain it (scale 1/√(κs), store), zero it, and release the MMA.
+//   fp32 input: the converter warps split a = hi + lo (two bf16) and the MMA runs
+//   twice (Φ is ±1, exact in bf16) — tf32 would miss the 1e-5 tolerance.
+// Outputs whose κ inputs straddle two CTAs' ranges are combined with red.global.add
+// into a zeroed Y; every such output has exactly two addends, so the result is still
+// bitwise deterministic (a+b == b+a in IEEE arithmetic).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
 #include "bps_internal.h"
+#include "bps_ptx.cuh"
+
 namespace bps {
-int tc_supported(const SketchParams&, int64_t, bps_dtype, bool, const Placement&) {
-  return fail(BPS_ERR_UNSUPPORTED, "tcgen05 variant not built yet");
+namespace {
+
+constexpr int kBK = 64;           // K rows per pipeline stage (one 128-byte swizzle row of bf16)
+constexpr int kBandTile = 128 * kBK * 2;  // one M-tile (128 band rows) of a band stage, bytes
+
+template <bool F32, bool TRANS, int NMT, int BN>
+struct Cfg {
+  static constexpr int ESZ = F32 ? 4 : 2;
+  static constexpr int RAW_STAGE = kBK * BN * ESZ;
+  static constexpr int NRAW = F32 ? (NMT == 1 ? 3 : 2) : 4;
+  static constexpr int CONV_HALF = kBK * BN * 2;
+  static constexpr int CONV_STAGE = F32 ? 2 * CONV_HALF : 0;
+  static constexpr int NCONV = F32 ? 2 : 0;
+  static constexpr int BAND_STAGE = NMT * kBandTile;
+  static constexpr int NBAND = F32 ? 2 : 3;
+  static constexpr int OFF_RAW = 0;
+  static constexpr int OFF_CONV = OFF_RAW + NRAW * RAW_STAGE;
+  static constexpr int OFF_BAND = OFF_CONV + NCONV * CONV_STAGE;
+  static constexpr int OFF_BAR = OFF_BAND + NBAND * BAND_STAGE;
+  // barriers: raw full/empty, conv full/empty, band full/empty, acc full/empty
+  static constexpr int NBARS = 2 * NRAW + 2 * NCONV + 2 * NBAND + 2;
+  static constexpr int OFF_GTAB = OFF_BAR + NBARS * 8;
+  static constexpr int OFF_TMEMPTR = OFF_GTAB + 2 * 256 * 4;
+  static constexpr int SMEM = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
+  static constexpr int NWARPS = F32 ? 16 : 12;          // 0 TMA, 1 MMA, 2-3 idle, 4-7 epi, 8-11 band, 12-15 conv
+  static constexpr int NTHREADS = NWARPS * 32;
+  static constexpr uint32_t TMEM_COLS = (NMT * BN <= 128) ? 128 : (NMT * BN <= 256 ? 256 : 512);
+  static constexpr uint32_t IDESC = ptx::idesc_bf16(128, BN, !TRANS);
+  static_assert(NMT * BN <= 512, "TMEM");
+  static_assert(SMEM <= 227 * 1024, "smem");
+};
+
+struct TcArgs {
+  SketchParams p;
+  int64_t n;         // columns of A (row-major) or vectors (transposed)
+  float* Y;
+  int64_t ldy;
+  int range_mode;
+  int64_t pos_begin, pos_end;  // owned outputs (range mode)
+  int64_t stream_begin;        // first input position of the launch window
+  int64_t stream_len;          // number of input positions in the window
+  int R;                       // ranges per column tile
+};
+
+__device__ __forceinline__ uint32_t mod_pos(int64_t i, uint32_t M) {
+  int64_t r = i % (int64_t)M;
+  return (uint32_t)(r < 0 ? r + M : r);
 }
-int launch_tc(const SketchParams&, const void*, int64_t, int64_t, bps_dtype, float*, int64_t, bool, const Placement&,
-              cudaStream_t) {
-  return fail(BPS_ERR_UNSUPPORTED, "tcgen05 variant not built yet");
+
+template <bool F32, bool TRANS, int NMT, int BN>
+__global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN>::NTHREADS, 1)
+    bps_tc_kernel(const __grid_constant__ CUtensorMap tmap, const TcArgs args) {
+  using K = Cfg<F32, TRANS, NMT, BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);
+  uint64_t* raw_full = bars;
+  uint64_t* raw_empty = raw_full + K::NRAW;
+  uint64_t* conv_full = raw_empty + K::NRAW;
+  uint64_t* conv_empty = conv_full + K::NCONV;
+  uint64_t* band_full = conv_empty + K::NCONV;
+  uint64_t* band_empty = band_full + K::NBAND;
+  uint64_t* acc_full = band_empty + K::NBAND;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* gtab = reinterpret_cast<uint32_t*>(smem + K::OFF_GTAB);
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + K::OFF_TMEMPTR);
+
+  const SketchParams& p = args.p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t kappa = p.kappa;
+  const int nk = (int)(p.B_c / kBK);
+
+  // ---- this CTA's column tile and input-position range
+  const int ct = blockIdx.x / args.R, rr = blockIdx.x % args.R;
+  const int64_t col0 = (int64_t)ct * BN;
+  const int64_t Lq = args.stream_len / args.R, Lrem = args.stream_len % args.R;
+  const int64_t P = args.stream_begin + rr * Lq + (rr < Lrem ? rr : Lrem);
+  const int64_t L = Lq + (rr < Lrem ? 1 : 0);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < K::NRAW; ++i) {
+      ptx::mbar_init(&raw_full[i], 1);
+      ptx::mbar_init(&raw_empty[i], F32 ? 128 : 1);
+    }
+    for (int i = 0; i < K::NCONV; ++i) {
+      ptx::mbar_init(&conv_full[i], 128);
+      ptx::mbar_init(&conv_empty[i], 1);
+    }
+    for (int i = 0; i < K::NBAND; ++i) {
+      ptx::mbar_init(&band_full[i], 128);
+      ptx::mbar_init(&band_empty[i], 1);
+    }
+    ptx::mbar_init(acc_full, 1);
+    ptx::mbar_init(acc_empty, 128);
+    ptx::fence_mbar_init();
+    ptx::tma_prefetch(&tmap);
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_ptr, K::TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+
+  // input block at absolute orbit position q -> first row in A (full: g_q·B_c; range: stacked)
+  auto in_row = [&](int64_t q, uint32_t gq) -> int64_t {
+    return args.range_mode ? (q - (args.pos_begin + 1)) * (int64_t)p.B_c : (int64_t)gq * p.B_c;
+  };
+
+  if (L > 0) {
+    if (warp == 0) {
+      // ===================== TMA producer =====================
+      if (lane == 0) {
+        const uint64_t pol = ptx::policy_evict_first();
+        uint32_t gq = affine_pow(p, (uint64_t)mod_pos(P, p.M), 0u);
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t q = P; q < P + L; ++q) {
+          const int64_t row0 = in_row(q, gq);
+          for (int kc = 0; kc < nk; ++kc) {
+            ptx::mbar_wait(&raw_empty[s], ph ^ 1);
+            ptx::mbar_arrive_expect_tx(&raw_full[s], K::RAW_STAGE);
+            uint8_t* dst = smem + K::OFF_RAW + s * K::RAW_STAGE;
+            const int32_t r = (int32_t)(row0 + kc * kBK);
+            if (!TRANS) {
+              if (F32) {
+                ptx::tma_load_2d(dst, &tmap, &raw_full[s], (int32_t)col0, r, pol);
+              } else {
+#pragma unroll
+                for (int b = 0; b < BN / 64; ++b)
+                  ptx::tma_load_2d(dst + b * (kBK * 128), &tmap, &raw_full[s], (int32_t)(col0 + 64 * b), r, pol);
+              }
+            } else {
+              ptx::tma_load_2d(dst, &tmap, &raw_full[s], r, (int32_t)col0, pol);
+            }
+            if (++s == K::NRAW) s = 0, ph ^= 1;
+          }
+          gq = affine_step(p, gq);
+        }
+      }
+    } else if (warp == 1) {
+      // ===================== MMA issuer =====================
+      if (lane == 0) {
+        int ds = 0, bs = 0;
+        uint32_t dph = 0, bph = 0, aph = 0;
+        uint64_t* dfull = F32 ? conv_full : raw_full;
+        uint64_t* dempty = F32 ? conv_empty : raw_empty;
+        constexpr int NDS = F32 ? K::NCONV : K::NRAW;
+        const uint32_t data_base = ptx::smem_u32(smem + (F32 ? K::OFF_CONV : K::OFF_RAW));
+        constexpr int DSTAGE = F32 ? K::CONV_STAGE : K::RAW_STAGE;
+        const uint32_t band_base = ptx::smem_u32(smem + K::OFF_BAND);
+        bool first = true;
+        for (int64_t q = P; q < P + L; ++q) {
+          if (q > P) {
+            ptx::mbar_wait(acc_empty, aph);
+            aph ^= 1;
+            ptx::tc_fence_after();
+          }
+          for (int kc = 0; kc < nk; ++kc) {
+            ptx::mbar_wait(&dfull[ds], dph);
+            ptx::mbar_wait(&band_full[bs], bph);
+            ptx::tc_fence_after();
+            const uint32_t dbase = data_base + ds * DSTAGE;
+            const uint32_t bbase = band_base + bs * K::BAND_STAGE;
+#pragma unroll
+            for (int ks = 0; ks < kBK / 16; ++ks) {
+#pragma unroll
+              for (int m = 0; m < NMT; ++m) {
+                const uint64_t adesc = ptx::smem_desc_sw128(bbase + m * kBandTile + ks * 32, 0, 1024);
+#pragma unroll
+                for (int part = 0; part < (F32 ? 2 : 1); ++part) {
+                  const uint32_t pb = dbase + part * (F32 ? K::CONV_HALF : 0);
+                  const uint64_t bdesc = TRANS ? ptx::smem_desc_sw128(pb + ks * 32, 0, 1024)
+                                               : ptx::smem_desc_sw128(pb + ks * 16 * 128, kBK * 128, 1024);
+                  const uint32_t acc = (first && ks == 0 && part == 0) ? 0u : 1u;
+                  ptx::mma_bf16_ss(tmem + m * BN, adesc, bdesc, K::IDESC, acc);
+                }
+              }
+              first = false;
+            }
+            ptx::mma_commit(&dempty[ds]);
+            ptx::mma_commit(&band_empty[bs]);
+            if (++ds == NDS) ds = 0, dph ^= 1;
+            if (++bs == K::NBAND) bs = 0, bph ^= 1;
+          }
+          ptx::mma_commit(acc_full);
+        }
+      }
+    } else if (warp >= 4 && warp < 8) {
+      // ===================== epilogue: drain / zero completed slots =====================
+      const int qtr = warp & 3;
+      uint32_t fph = 0;
+      auto drain = [&](int64_t i, bool zero) {
+        const uint32_t slot = mod_pos(i, kappa);
+        const uint32_t lo = slot * p.B_r, hi = lo + p.B_r;
+        const bool owned = args.range_mode ? (i >= args.pos_begin && i < args.pos_end) : true;
+        const bool complete = (i + 1 >= P) && (i + (int64_t)kappa <= P + L - 1);
+        int64_t out_row0 = 0;
+        if (owned)
+          out_row0 = args.range_mode ? (i - args.pos_begin) * (int64_t)p.B_r
+                                     : (int64_t)affine_pow(p, (uint64_t)mod_pos(i, p.M), 0u) * p.B_r;
+#pragma unroll 1
+        for (int m = 0; m < NMT; ++m) {
+          const uint32_t qlo = m * 128 + qtr * 32;
+          if (qlo + 32 <= lo || qlo >= hi) continue;  // warp-uniform
+          const uint32_t rho = qlo + lane;
+          const bool in_slot = rho >= lo && rho < hi;
+          const int64_t row = out_row0 + (int64_t)rho - lo;
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t v[32];
+            const uint32_t taddr = tmem + ((uint32_t)(qtr * 32) << 16) + (uint32_t)(m * BN + c0);
+            ptx::tmem_ld32(taddr, v);
+            ptx::tmem_wait_ld();
+            if (in_slot && owned) {
+              const int64_t cbase = col0 + c0;
+              if (!TRANS) {
+                float* y = args.Y + row * args.ldy + cbase;
+#pragma unroll
+                for (int t = 0; t < 32; t += 4) {
+                  const float a0 = __uint_as_float(v[t]) * p.scale, a1 = __uint_as_float(v[t + 1]) * p.scale;
+                  const float a2 = __uint_as_float(v[t + 2]) * p.scale, a3 = __uint_as_float(v[t + 3]) * p.scale;
+                  if (cbase + t + 3 < args.n) {
+                    if (complete)
+                      *reinterpret_cast<float4*>(y + t) = make_float4(a0, a1, a2, a3);
+                    else
+                      ptx::red_add_v4(y + t, a0, a1, a2, a3);
+                  } else {
+                    const float a[4] = {a0, a1, a2, a3};
+                    for (int e = 0; e < 4; ++e)
+                      if (cbase + t + e < args.n) {
+                        if (complete) y[t + e] = a[e];
+                        else ptx::red_add(y + t + e, a[e]);
+                      }
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                  if (cbase + t < args.n) {
+                    float* y = args.Y + (cbase + t) * args.ldy + row;
+                    const float a = __uint_as_float(v[t]) * p.scale;
+                    if (complete) *y = a;
+                    else ptx::red_add(y, a);
+                  }
+                }
+              }
+            }
+            if (zero) {
+#pragma unroll
+              for (int t = 0; t < 32; ++t) v[t] = in_slot ? 0u : v[t];
+              ptx::tmem_st32(taddr, v);
+            }
+          }
+          if (zero) ptx::tmem_wait_st();
+        }
+      };
+      for (int64_t q = P; q < P + L; ++q) {
+        ptx::mbar_wait(acc_full, fph);
+        fph ^= 1;
+        ptx::tc_fence_after();
+        drain(q - (int64_t)kappa, true);
+        if (q == P + L - 1)
+          for (int64_t i = P + L - (int64_t)kappa; i <= P + L - 2; ++i) drain(i, false);
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(acc_empty);
+      }
+    } else if (warp >= 8 && warp < 12) {
+      // ===================== band generator =====================
+      const int bt = threadIdx.x - 256;
+      int bs = 0;
+      uint32_t bph = 0;
+      const uint32_t E = kappa * p.s * kBK;
+      for (int64_t q = P; q < P + L; ++q) {
+        uint32_t* gt = gtab + (q & 1) * 256;
+        const uint32_t qmod = mod_pos(q, kappa);
+        for (int kc = 0; kc < nk; ++kc) {
+          ptx::mbar_wait(&band_empty[bs], bph ^ 1);
+          if (kc == 0 && bt == 0) {
+            uint32_t g = affine_pow(p, (uint64_t)mod_pos(q - (int64_t)kappa, p.M), 0u);  // g_{q-κ}
+            for (int l = (int)kappa; l >= 1; --l) {
+              gt[l - 1] = g;  // g_{q-l}
+              g = affine_step(p, g);
+            }
+          }
+          uint8_t* band = smem + K::OFF_BAND + bs * K::BAND_STAGE;
+          uint4* bz = reinterpret_cast<uint4*>(band);
+          for (int i = bt; i < K::BAND_STAGE / 16; i += 128) bz[i] = make_uint4(0, 0, 0, 0);
+          ptx::named_bar_sync(1, 128);
+          const uint32_t u0 = (uint32_t)kc * kBK;
+          for (uint32_t e = bt; e < E; e += 128) {
+            const uint32_t u = e % kBK;
+            const uint32_t lj = e / kBK;
+            const uint32_t j = lj % p.s;
+            const uint32_t ell = lj / p.s + 1;
+            const uint32_t g = gt[ell - 1];
+            const Draw dr = pattern(p, g, ell, u0 + u, j);
+            const uint32_t slot = (qmod + kappa - (ell % kappa)) % kappa;  // (q - ℓ) mod κ
+            const uint32_t rho = slot * p.B_r + dr.row;
+            const uint32_t m = rho >> 7, r7 = rho & 127;
+            const uint32_t off = m * kBandTile + (r7 >> 3) * 1024 + (r7 & 7) * 128 + (((u >> 3) ^ (r7 & 7)) << 4) +
+                                 (u & 7) * 2;
+            *reinterpret_cast<uint16_t*>(band + off) = dr.neg ? 0xBF80u : 0x3F80u;
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(&band_full[bs]);
+          if (++bs == K::NBAND) bs = 0, bph ^= 1;
+        }
+      }
+    } else if (F32 && warp >= 12) {
+      // ===================== fp32 -> (hi, lo) bf16 split =====================
+      const int cv = threadIdx.x - 384;
+      int rs = 0, cs = 0;
+      uint32_t rph = 0, cph = 0;
+      const int64_t total = L * nk;
+      for (int64_t it = 0; it < total; ++it) {
+        ptx::mbar_wait(&raw_full[rs], rph);
+        ptx::mbar_wait(&conv_empty[cs], cph ^ 1);
+        const float* raw = reinterpret_cast<const float*>(smem + K::OFF_RAW + rs * K::RAW_STAGE);
+        uint8_t* hi = smem + K::OFF_CONV + cs * K::CONV_STAGE;
+        uint8_t* lo = hi + K::CONV_HALF;
+#pragma unroll 4
+        for (int idx = cv; idx < kBK * BN / 4; idx += 128) {
+          int rowk, c;  // (K index, MN index) of the first of 4 consecutive elements
+          uint32_t off;
+          if (!TRANS) {
+            rowk = idx / (BN / 4);
+            c = (idx % (BN / 4)) * 4;  // column
+            const int blk = c >> 6, cc = c & 63;
+            off = blk * (kBK * 128) + (rowk >> 3) * 1024 + (rowk & 7) * 128 + ((((cc >> 3) ^ (rowk & 7))) << 4) +
+                  (cc & 7) * 2;
+          } else {
+            const int v = idx / (kBK / 4);  // vector (MN)
+            c = (idx % (kBK / 4)) * 4;      // coordinate (K)
+            rowk = v;
+            off = (v >> 3) * 1024 + (v & 7) * 128 + ((((c >> 3) ^ (v & 7))) << 4) + (c & 7) * 2;
+          }
+          const float4 a = *reinterpret_cast<const float4*>(raw + (size_t)idx * 4);
+          const __nv_bfloat162 h01 = __floats2bfloat162_rn(a.x, a.y);
+          const __nv_bfloat162 h23 = __floats2bfloat162_rn(a.z, a.w);
+          const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+          const __nv_bfloat162 l01 = __floats2bfloat162_rn(a.x - f01.x, a.y - f01.y);
+          const __nv_bfloat162 l23 = __floats2bfloat162_rn(a.z - f23.x, a.w - f23.y);
+          uint2 hv, lv;
+          hv.x = *reinterpret_cast<const uint32_t*>(&h01);
+          hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+          lv.x = *reinterpret_cast<const uint32_t*>(&l01);
+          lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+          *reinterpret_cast<uint2*>(hi + off) = hv;
+          *reinterpret_cast<uint2*>(lo + off) = lv;
+          (void)rowk;
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&raw_empty[rs]);
+        ptx::mbar_arrive(&conv_full[cs]);
+        if (++rs == K::NRAW) rs = 0, rph ^= 1;
+        if (++cs == K::NCONV) cs = 0, cph ^= 1;
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, K::TMEM_COLS);
+  }
 }
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  }
+  return fn;
+}
+
+struct Plan {
+  bool ok = false;
+  int nmt = 1, bn = 128;
+  std::string why;
+};
+
+Plan plan_for(const SketchParams& p, bps_dtype dt) {
+  Plan pl;
+  if (dt != BPS_F32 && dt != BPS_BF16) {
+    pl.why = "dtype";
+    return pl;
+  }
+  if (p.B_c % kBK != 0) {
+    pl.why = "tc variant needs B_c % 64 == 0";
+    return pl;
+  }
+  const uint64_t rows = (uint64_t)p.kappa * p.B_r;
+  if (rows > 256) {
+    pl.why = "tc variant needs kappa*B_r <= 256";
+    return pl;
+  }
+  pl.nmt = rows <= 128 ? 1 : 2;
+  pl.bn = (dt == BPS_BF16 && pl.nmt == 1) ? 256 : 128;
+  pl.ok = true;
+  return pl;
+}
+
+template <bool F32, bool TRANS, int NMT, int BN>
+int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, float* Y, int64_t ldy,
+                const Placement& pl, cudaStream_t st) {
+  using K = Cfg<F32, TRANS, NMT, BN>;
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(BPS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
+  // geometry of the launch window
+  TcArgs a;
+  a.p = p;
+  a.n = n;
+  a.Y = Y;
+  a.ldy = ldy;
+  a.range_mode = pl.range_mode;
+  a.pos_begin = pl.pos_begin;
+  a.pos_end = pl.pos_begin + pl.n_out;
+  int64_t in_rows;
+  if (pl.range_mode) {
+    a.stream_begin = pl.pos_begin + 1;
+    a.stream_len = pl.n_out + p.kappa - 1;
+    in_rows = a.stream_len * (int64_t)p.B_c;
+  } else {
+    a.stream_begin = 1;
+    a.stream_len = p.M;
+    in_rows = (int64_t)p.M * p.B_c;
+  }
+  const int64_t n_ct = (n + BN - 1) / BN;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t R = n_ct >= sms ? 1 : sms / n_ct;
+  if (R > a.stream_len) R = a.stream_len;
+  const int64_t need = p.kappa > 1 ? (int64_t)p.kappa - 1 : 1;
+  while (R > 1 && a.stream_len / R < need) --R;  // ≤ 2 contributors per split output
+  a.R = (int)R;
+  const int64_t grid = n_ct * R;
+  if (grid > 0x7FFFFFFF) return fail(BPS_ERR_UNSUPPORTED, "grid too large");
+  if (in_rows > 0x7FFFFFFF || n > 0x7FFFFFFF) return fail(BPS_ERR_UNSUPPORTED, "tc variant: TMA coordinates exceed int32");
+
+  // TMA descriptor for the data operand
+  CUtensorMap tm;
+  const CUtensorMapDataType tdt = F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  cuuint64_t dims[2], strides[1];
+  cuuint32_t box[2], estr[2] = {1, 1};
+  CUtensorMapSwizzle swz;
+  if (!TRANS) {
+    dims[0] = (cuuint64_t)n;
+    dims[1] = (cuuint64_t)in_rows;
+    strides[0] = (cuuint64_t)lda * K::ESZ;
+    box[0] = F32 ? BN : 64;
+    box[1] = kBK;
+    swz = F32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B;
+  } else {
+    dims[0] = (cuuint64_t)in_rows;  // coordinates (d)
+    dims[1] = (cuuint64_t)n;        // vectors
+    strides[0] = (cuuint64_t)lda * K::ESZ;
+    box[0] = kBK;
+    box[1] = BN;
+    swz = F32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B;
+  }
+  CUresult cr = enc(&tm, tdt, 2, const_cast<void*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(BPS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+
+  // outputs split between two CTAs are accumulated with red.add into a zeroed Y
+  if (p.kappa > 1) {
+    cudaError_t e = TRANS ? cudaMemset2DAsync(Y, ldy * 4, 0, (size_t)(pl.range_mode ? pl.n_out * p.B_r : (int64_t)p.M * p.B_r) * 4, n, st)
+                          : cudaMemset2DAsync(Y, ldy * 4, 0, (size_t)n * 4, (size_t)(pl.n_out * p.B_r), st);
+    if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaMemset2DAsync: ") + cudaGetErrorString(e));
+  }
+  auto kern = bps_tc_kernel<F32, TRANS, NMT, BN>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+  if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  kern<<<(unsigned)grid, K::NTHREADS, K::SMEM, st>>>(tm, a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("bps_tc_kernel launch: ") + cudaGetErrorString(e));
+  return BPS_OK;
+}
+
+}  // namespace
+
+int tc_supported(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl) {
+  (void)n;
+  (void)transposed;
+  (void)pl;
+  Plan plan = plan_for(p, dt);
+  if (!plan.ok) return fail(BPS_ERR_UNSUPPORTED, plan.why);
+  return BPS_OK;
+}
+
+int launch_tc(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt, float* Y, int64_t ldy,
+              bool transposed, const Placement& pl, cudaStream_t st) {
+  Plan plan = plan_for(p, dt);
+  if (!plan.ok) return fail(BPS_ERR_UNSUPPORTED, plan.why);
+  const bool f32 = dt == BPS_F32;
+#define BPS_TC_CASE(F, T, NM, B)                                                 \
+  if (f32 == F && transposed == T && plan.nmt == NM && plan.bn == B)           \
+    return launch_impl<F, T, NM, B>(p, A, lda, n, Y, ldy, pl, st);
+  BPS_TC_CASE(true, false, 1, 128)
+  BPS_TC_CASE(true, false, 2, 128)
+  BPS_TC_CASE(true, true, 1, 128)
+  BPS_TC_CASE(true, true, 2, 128)
+  BPS_TC_CASE(false, false, 1, 256)
+  BPS_TC_CASE(false, false, 2, 128)
+  BPS_TC_CASE(false, true, 1, 256)
+  BPS_TC_CASE(false, true, 2, 128)
+#undef BPS_TC_CASE
+  return fail(BPS_ERR_UNSUPPORTED, "no tc instantiation for this plan");
+}
+
 }  // namespace bps

@@ -19,11 +19,23 @@ from paper_2602_06071_b200 import configs as C  # noqa: E402
 VARIANTS = ["sparse", "tc"]
 
 
+def _padded(rows, cols, dtype, fill=None):
+    """rows×cols view with a 16-byte-aligned leading dimension (ABI alignment rule)."""
+    mult = 16 // torch.tensor([], dtype=dtype).element_size()
+    ld = max(mult, -(-cols // mult) * mult)
+    base = torch.zeros((rows, ld), dtype=dtype, device="cuda")
+    v = base[:, :cols]
+    if fill is not None:
+        v.copy_(fill)
+    return v
+
+
 def _run(sk, A_host, variant, dtype=torch.float32, transposed=False):
-    dev = torch.device("cuda")
-    A = torch.from_numpy(np.ascontiguousarray(A_host)).to(dev).to(dtype)
+    A_src = torch.from_numpy(np.ascontiguousarray(A_host)).cuda().to(dtype)
+    A = _padded(A_src.shape[0], A_src.shape[1], dtype, A_src)
+    out = _padded(A.shape[0], sk.k, torch.float32) if transposed else _padded(sk.k, A.shape[1], torch.float32)
     try:
-        Y = sk.apply_t(A, variant=variant) if transposed else sk.apply(A, variant=variant)
+        Y = sk.apply_t(A, out=out, variant=variant) if transposed else sk.apply(A, out=out, variant=variant)
     except BpsError as e:
         if e.code == -3 and variant == "tc":
             pytest.skip(f"tc variant does not cover this shape: {e}")
