@@ -9,9 +9,13 @@
 // rotated so output i always lands in slot i mod κ) from the counter hash (R2) and
 // feeds it to tcgen05.mma as the K-major A operand; the data tile (TMA, SW128) is
 // the B operand (MN-major for row-major A, K-major for the transposed layout).
-// D (TMEM, fp32) rows = band rows, columns = data columns; the κ slots accumulate
-// across input blocks, and after block p the slot of output p−κ is complete: the
-// epilogue warps drain it (scale 1/√(κs), store), zero it, and release the MMA.
+// D (TMEM, fp32) rows = band rows, columns = data columns.  Accumulation: the tensor
+// core's fp32 accumulate is not round-to-nearest (measured: error grows ∝ #MMAs ×
+// |acc|), so D is fresh for every group of G·64 input rows (two buffers D0/D1
+// alternate) and the epilogue warps fold each group into a TMEM running sum S with
+// IEEE round-to-nearest fp32 adds on the CUDA cores.  The κ slots of S hold the κ
+// outputs in flight; after the last group of input block p the slot of output p−κ is
+// complete: it is scaled by 1/√(κs), stored, and zeroed.
 //   fp32 input: the converter warps split a = hi + lo (two bf16) and the MMA runs
 //   twice (Φ is ±1, exact in bf16) — tf32 would miss the 1e-5 tolerance.
 // Outputs whose κ inputs straddle two CTAs' ranges are combined with red.global.add
@@ -29,33 +33,39 @@
 namespace bps {
 namespace {
 
-constexpr int kBK = 64;           // K rows per pipeline stage (one 128-byte swizzle row of bf16)
+constexpr int kBK = 64;                   // K rows per pipeline stage (one 128-byte swizzle row of bf16)
 constexpr int kBandTile = 128 * kBK * 2;  // one M-tile (128 band rows) of a band stage, bytes
+constexpr int kMaxCombos = 256;           // κ·s ≤ κ·B_r ≤ 256 on this path
 
-template <bool F32, bool TRANS, int NMT, int BN>
+// Warp roles: 0 TMA producer | 1 MMA issuer (+TMEM alloc) | 2-3 idle | 4-7 epilogue
+// (TMEM lane quarters 0-3) | 8-15 band generator | 16-19 fp32 hi/lo converter (fp32 only).
+template <bool F32, bool TRANS, int NMT>
 struct Cfg {
+  static constexpr int BN = 128 / NMT;  // data columns per CTA; TMEM = D0, D1, S each NMT·BN columns
   static constexpr int ESZ = F32 ? 4 : 2;
   static constexpr int RAW_STAGE = kBK * BN * ESZ;
-  static constexpr int NRAW = F32 ? (NMT == 1 ? 3 : 2) : 4;
+  static constexpr int NRAW = F32 ? (NMT == 1 ? 3 : 4) : (NMT == 1 ? 6 : 8);
   static constexpr int CONV_HALF = kBK * BN * 2;
   static constexpr int CONV_STAGE = F32 ? 2 * CONV_HALF : 0;
   static constexpr int NCONV = F32 ? 2 : 0;
   static constexpr int BAND_STAGE = NMT * kBandTile;
-  static constexpr int NBAND = F32 ? 2 : 3;
+  static constexpr int NBAND = (NMT == 1 && !F32) ? 3 : 2;
   static constexpr int OFF_RAW = 0;
   static constexpr int OFF_CONV = OFF_RAW + NRAW * RAW_STAGE;
   static constexpr int OFF_BAND = OFF_CONV + NCONV * CONV_STAGE;
-  static constexpr int OFF_BAR = OFF_BAND + NBAND * BAND_STAGE;
-  // barriers: raw full/empty, conv full/empty, band full/empty, acc full/empty
-  static constexpr int NBARS = 2 * NRAW + 2 * NCONV + 2 * NBAND + 2;
-  static constexpr int OFF_GTAB = OFF_BAR + NBARS * 8;
-  static constexpr int OFF_TMEMPTR = OFF_GTAB + 2 * 256 * 4;
+  static constexpr int OFF_CKEY = OFF_BAND + NBAND * BAND_STAGE;   // [2][kMaxCombos] u64
+  static constexpr int OFF_CROW = OFF_CKEY + 2 * kMaxCombos * 8;   // [2][kMaxCombos] u32
+  static constexpr int OFF_BAR = OFF_CROW + 2 * kMaxCombos * 4;
+  // raw full/empty, conv full/empty, band full/empty, acc full[2], acc free[2]
+  static constexpr int NBARS = 2 * NRAW + 2 * NCONV + 2 * NBAND + 4;
+  static constexpr int OFF_TMEMPTR = OFF_BAR + NBARS * 8;
   static constexpr int SMEM = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
-  static constexpr int NWARPS = F32 ? 16 : 12;          // 0 TMA, 1 MMA, 2-3 idle, 4-7 epi, 8-11 band, 12-15 conv
+  static constexpr int NWARPS = F32 ? 20 : 16;
   static constexpr int NTHREADS = NWARPS * 32;
-  static constexpr uint32_t TMEM_COLS = (NMT * BN <= 128) ? 128 : (NMT * BN <= 256 ? 256 : 512);
+  static constexpr int NBANDT = 256;  // band generator threads
+  static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t IDESC = ptx::idesc_bf16(128, BN, !TRANS);
-  static_assert(NMT * BN <= 512, "TMEM");
+  static_assert(3 * NMT * BN <= 512, "TMEM");
   static_assert(SMEM <= 227 * 1024, "smem");
 };
 
@@ -69,6 +79,7 @@ struct TcArgs {
   int64_t stream_begin;        // first input position of the launch window
   int64_t stream_len;          // number of input positions in the window
   int R;                       // ranges per column tile
+  int G;                       // K-chunks per accumulation group (divides B_c/64)
 };
 
 __device__ __forceinline__ uint32_t mod_pos(int64_t i, uint32_t M) {
@@ -76,12 +87,13 @@ __device__ __forceinline__ uint32_t mod_pos(int64_t i, uint32_t M) {
   return (uint32_t)(r < 0 ? r + M : r);
 }
 
-template <bool F32, bool TRANS, int NMT, int BN>
-__global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN>::NTHREADS, 1)
+template <bool F32, bool TRANS, int NMT>
+__global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
     bps_tc_kernel(const __grid_constant__ CUtensorMap tmap, const TcArgs args) {
-  using K = Cfg<F32, TRANS, NMT, BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using K = Cfg<F32, TRANS, NMT>;
+  constexpr int BN = K::BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = raw_full + K::NRAW;
@@ -89,15 +101,17 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN>::NTHREADS, 1)
   uint64_t* conv_empty = conv_full + K::NCONV;
   uint64_t* band_full = conv_empty + K::NCONV;
   uint64_t* band_empty = band_full + K::NBAND;
-  uint64_t* acc_full = band_empty + K::NBAND;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* gtab = reinterpret_cast<uint32_t*>(smem + K::OFF_GTAB);
+  uint64_t* acc_full = band_empty + K::NBAND;  // [2]
+  uint64_t* acc_free = acc_full + 2;           // [2]
+  uint64_t* ckey = reinterpret_cast<uint64_t*>(smem + K::OFF_CKEY);
+  uint32_t* crow = reinterpret_cast<uint32_t*>(smem + K::OFF_CROW);
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + K::OFF_TMEMPTR);
 
   const SketchParams& p = args.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t kappa = p.kappa;
   const int nk = (int)(p.B_c / kBK);
+  const int G = args.G;
 
   // ---- this CTA's column tile and input-position range
   const int ct = blockIdx.x / args.R, rr = blockIdx.x % args.R;
@@ -116,11 +130,13 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN>::NTHREADS, 1)
       ptx::mbar_init(&conv_empty[i], 1);
     }
     for (int i = 0; i < K::NBAND; ++i) {
-      ptx::mbar_init(&band_full[i], 128);
+      ptx::mbar_init(&band_full[i], K::NBANDT);
       ptx::mbar_init(&band_empty[i], 1);
     }
-    ptx::mbar_init(acc_full, 1);
-    ptx::mbar_init(acc_empty, 128);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&acc_full[i], 1);
+      ptx::mbar_init(&acc_free[i], 128);
+    }
     ptx::fence_mbar_init();
     ptx::tma_prefetch(&tmap);
   }
@@ -129,11 +145,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN>::NTHREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_ptr;
-
-  // input block at absolute orbit position q -> first row in A (full: g_q·B_c; range: stacked)
-  auto in_row = [&](int64_t q, uint32_t gq) -> int64_t {
-    return args.range_mode ? (q - (args.pos_begin + 1)) * (int64_t)p.B_c : (int64_t)gq * p.B_c;
-  };
+  const uint32_t tmem_S = tmem + 2 * NMT * BN;  // fp32 running sums (RN adds on CUDA cores)
 
   if (L > 0) {
     if (warp == 0) {
@@ -144,7 +156,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN>::NTHREADS, 1)
         int s = 0;
         uint32_t ph = 0;
         for (int64_t q = P; q < P + L; ++q) {
-          const int64_t row0 = in_row(q, gq);
+          const int64_t row0 = args.range_mode ? (q - (args.pos_begin + 1)) * (int64_t)p.B_c : (int64_t)gq * p.B_c;
           for (int kc = 0; kc < nk; ++kc) {
             ptx::mbar_wait(&raw_empty[s], ph ^ 1);
             ptx::mbar_arrive_expect_tx(&raw_full[s], K::RAW_STAGE);
@@ -170,26 +182,30 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN>::NTHREADS, 1)
       // ===================== MMA issuer =====================
       if (lane == 0) {
         int ds = 0, bs = 0;
-        uint32_t dph = 0, bph = 0, aph = 0;
+        uint32_t dph = 0, bph = 0;
+        uint32_t fbits = 0;  // phase bit per accumulator buffer
+        uint32_t grp = 0;
         uint64_t* dfull = F32 ? conv_full : raw_full;
         uint64_t* dempty = F32 ? conv_empty : raw_empty;
         constexpr int NDS = F32 ? K::NCONV : K::NRAW;
         const uint32_t data_base = ptx::smem_u32(smem + (F32 ? K::OFF_CONV : K::OFF_RAW));
         constexpr int DSTAGE = F32 ? K::CONV_STAGE : K::RAW_STAGE;
         const uint32_t band_base = ptx::smem_u32(smem + K::OFF_BAND);
-        bool first = true;
         for (int64_t q = P; q < P + L; ++q) {
-          if (q > P) {
-            ptx::mbar_wait(acc_empty, aph);
-            aph ^= 1;
-            ptx::tc_fence_after();
-          }
           for (int kc = 0; kc < nk; ++kc) {
+            const int gi = kc % G;
+            const uint32_t buf = grp & 1;
+            if (gi == 0 && grp >= 2) {  // accumulator buffer must have been flushed into S
+              ptx::mbar_wait(&acc_free[buf], (fbits >> buf) & 1u);
+              fbits ^= 1u << buf;
+              ptx::tc_fence_after();
+            }
             ptx::mbar_wait(&dfull[ds], dph);
             ptx::mbar_wait(&band_full[bs], bph);
             ptx::tc_fence_after();
             const uint32_t dbase = data_base + ds * DSTAGE;
             const uint32_t bbase = band_base + bs * K::BAND_STAGE;
+            const uint32_t dacc = tmem + buf * (NMT * BN);
 #pragma unroll
             for (int ks = 0; ks < kBK / 16; ++ks) {
 #pragma unroll
@@ -200,144 +216,181 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN>::NTHREADS, 1)
                   const uint32_t pb = dbase + part * (F32 ? K::CONV_HALF : 0);
                   const uint64_t bdesc = TRANS ? ptx::smem_desc_sw128(pb + ks * 32, 0, 1024)
                                                : ptx::smem_desc_sw128(pb + ks * 16 * 128, kBK * 128, 1024);
-                  const uint32_t acc = (first && ks == 0 && part == 0) ? 0u : 1u;
-                  ptx::mma_bf16_ss(tmem + m * BN, adesc, bdesc, K::IDESC, acc);
+                  const uint32_t acc = (gi == 0 && ks == 0 && part == 0) ? 0u : 1u;  // fresh per group
+                  ptx::mma_bf16_ss(dacc + m * BN, adesc, bdesc, K::IDESC, acc);
                 }
               }
-              first = false;
             }
             ptx::mma_commit(&dempty[ds]);
             ptx::mma_commit(&band_empty[bs]);
             if (++ds == NDS) ds = 0, dph ^= 1;
             if (++bs == K::NBAND) bs = 0, bph ^= 1;
+            if (gi == G - 1) {
+              ptx::mma_commit(&acc_full[buf]);
+              ++grp;
+            }
           }
-          ptx::mma_commit(acc_full);
         }
       }
     } else if (warp >= 4 && warp < 8) {
-      // ===================== epilogue: drain / zero completed slots =====================
+      // ============ epilogue: S += D (fp32 RN) per group; emit the slot that completes ============
       const int qtr = warp & 3;
-      uint32_t fph = 0;
-      auto drain = [&](int64_t i, bool zero) {
-        const uint32_t slot = mod_pos(i, kappa);
-        const uint32_t lo = slot * p.B_r, hi = lo + p.B_r;
+      const uint32_t lane_off = (uint32_t)(qtr * 32) << 16;
+      {  // S = 0
+        uint32_t z[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) z[t] = 0u;
+        for (int c = 0; c < NMT * BN; c += 16) ptx::tmem_st16(tmem_S + lane_off + c, z);
+        ptx::tmem_wait_st();
+      }
+      auto emit = [&](int64_t i, int m, uint32_t rho, const float* vals, int c0) {
+        // vals: 16 S values of output row (rho - slot lo) of output i, columns col0+c0..+15
         const bool owned = args.range_mode ? (i >= args.pos_begin && i < args.pos_end) : true;
+        if (!owned) return;
+        const uint32_t lo = mod_pos(i, kappa) * p.B_r;
         const bool complete = (i + 1 >= P) && (i + (int64_t)kappa <= P + L - 1);
-        int64_t out_row0 = 0;
-        if (owned)
-          out_row0 = args.range_mode ? (i - args.pos_begin) * (int64_t)p.B_r
-                                     : (int64_t)affine_pow(p, (uint64_t)mod_pos(i, p.M), 0u) * p.B_r;
-#pragma unroll 1
-        for (int m = 0; m < NMT; ++m) {
-          const uint32_t qlo = m * 128 + qtr * 32;
-          if (qlo + 32 <= lo || qlo >= hi) continue;  // warp-uniform
-          const uint32_t rho = qlo + lane;
-          const bool in_slot = rho >= lo && rho < hi;
-          const int64_t row = out_row0 + (int64_t)rho - lo;
-#pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 32) {
-            uint32_t v[32];
-            const uint32_t taddr = tmem + ((uint32_t)(qtr * 32) << 16) + (uint32_t)(m * BN + c0);
-            ptx::tmem_ld32(taddr, v);
-            ptx::tmem_wait_ld();
-            if (in_slot && owned) {
-              const int64_t cbase = col0 + c0;
-              if (!TRANS) {
-                float* y = args.Y + row * args.ldy + cbase;
+        const int64_t row = (args.range_mode ? (i - args.pos_begin) * (int64_t)p.B_r
+                                             : (int64_t)affine_pow(p, (uint64_t)mod_pos(i, p.M), 0u) * p.B_r) +
+                            (int64_t)(rho - lo);
+        const int64_t cbase = col0 + c0;
+        (void)m;
+        if (!TRANS) {
+          float* y = args.Y + row * args.ldy + cbase;
 #pragma unroll
-                for (int t = 0; t < 32; t += 4) {
-                  const float a0 = __uint_as_float(v[t]) * p.scale, a1 = __uint_as_float(v[t + 1]) * p.scale;
-                  const float a2 = __uint_as_float(v[t + 2]) * p.scale, a3 = __uint_as_float(v[t + 3]) * p.scale;
-                  if (cbase + t + 3 < args.n) {
-                    if (complete)
-                      *reinterpret_cast<float4*>(y + t) = make_float4(a0, a1, a2, a3);
-                    else
-                      ptx::red_add_v4(y + t, a0, a1, a2, a3);
-                  } else {
-                    const float a[4] = {a0, a1, a2, a3};
-                    for (int e = 0; e < 4; ++e)
-                      if (cbase + t + e < args.n) {
-                        if (complete) y[t + e] = a[e];
-                        else ptx::red_add(y + t + e, a[e]);
-                      }
-                  }
+          for (int t = 0; t < 16; t += 4) {
+            const float a0 = vals[t] * p.scale, a1 = vals[t + 1] * p.scale;
+            const float a2 = vals[t + 2] * p.scale, a3 = vals[t + 3] * p.scale;
+            if (cbase + t + 3 < args.n) {
+              if (complete) *reinterpret_cast<float4*>(y + t) = make_float4(a0, a1, a2, a3);
+              else ptx::red_add_v4(y + t, a0, a1, a2, a3);
+            } else {
+              const float a[4] = {a0, a1, a2, a3};
+              for (int e = 0; e < 4; ++e)
+                if (cbase + t + e < args.n) {
+                  if (complete) y[t + e] = a[e];
+                  else ptx::red_add(y + t + e, a[e]);
                 }
-              } else {
-#pragma unroll
-                for (int t = 0; t < 32; ++t) {
-                  if (cbase + t < args.n) {
-                    float* y = args.Y + (cbase + t) * args.ldy + row;
-                    const float a = __uint_as_float(v[t]) * p.scale;
-                    if (complete) *y = a;
-                    else ptx::red_add(y, a);
-                  }
-                }
-              }
-            }
-            if (zero) {
-#pragma unroll
-              for (int t = 0; t < 32; ++t) v[t] = in_slot ? 0u : v[t];
-              ptx::tmem_st32(taddr, v);
             }
           }
-          if (zero) ptx::tmem_wait_st();
+        } else {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            if (cbase + t < args.n) {
+              float* y = args.Y + (cbase + t) * args.ldy + row;
+              const float a = vals[t] * p.scale;
+              if (complete) *y = a;
+              else ptx::red_add(y, a);
+            }
+          }
         }
       };
+      uint32_t abits = 0;  // phase bit per accumulator buffer
+      uint32_t grp = 0;
+      const int ngrp = nk / G;
       for (int64_t q = P; q < P + L; ++q) {
-        ptx::mbar_wait(acc_full, fph);
-        fph ^= 1;
-        ptx::tc_fence_after();
-        drain(q - (int64_t)kappa, true);
-        if (q == P + L - 1)
-          for (int64_t i = P + L - (int64_t)kappa; i <= P + L - 2; ++i) drain(i, false);
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(acc_empty);
-      }
-    } else if (warp >= 8 && warp < 12) {
-      // ===================== band generator =====================
-      const int bt = threadIdx.x - 256;
-      int bs = 0;
-      uint32_t bph = 0;
-      const uint32_t E = kappa * p.s * kBK;
-      for (int64_t q = P; q < P + L; ++q) {
-        uint32_t* gt = gtab + (q & 1) * 256;
-        const uint32_t qmod = mod_pos(q, kappa);
-        for (int kc = 0; kc < nk; ++kc) {
-          ptx::mbar_wait(&band_empty[bs], bph ^ 1);
-          if (kc == 0 && bt == 0) {
-            uint32_t g = affine_pow(p, (uint64_t)mod_pos(q - (int64_t)kappa, p.M), 0u);  // g_{q-κ}
-            for (int l = (int)kappa; l >= 1; --l) {
-              gt[l - 1] = g;  // g_{q-l}
-              g = affine_step(p, g);
+        for (int gix = 0; gix < ngrp; ++gix, ++grp) {
+          const uint32_t buf = grp & 1;
+          ptx::mbar_wait(&acc_full[buf], (abits >> buf) & 1u);
+          abits ^= 1u << buf;
+          ptx::tc_fence_after();
+          const bool last = gix == ngrp - 1;
+          const int64_t i = q - (int64_t)kappa;  // output completed by input block q
+          const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
+#pragma unroll 1
+          for (int m = 0; m < NMT; ++m) {
+            const uint32_t rho = m * 128 + qtr * 32 + lane;
+            const bool quarter_hit = last && !(m * 128 + qtr * 32 + 32 <= lo || m * 128 + qtr * 32 >= hi);
+            const bool in_slot = last && rho >= lo && rho < hi;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              uint32_t d[16], sv[16];
+              ptx::tmem_ld16(tmem + buf * (NMT * BN) + lane_off + m * BN + c0, d);
+              ptx::tmem_ld16(tmem_S + lane_off + m * BN + c0, sv);
+              ptx::tmem_wait_ld();
+              float tot[16];
+#pragma unroll
+              for (int t = 0; t < 16; ++t) tot[t] = __uint_as_float(sv[t]) + __uint_as_float(d[t]);
+              if (quarter_hit && in_slot) emit(i, m, rho, tot, c0);
+#pragma unroll
+              for (int t = 0; t < 16; ++t) sv[t] = in_slot ? 0u : __float_as_uint(tot[t]);
+              ptx::tmem_st16(tmem_S + lane_off + m * BN + c0, sv);
             }
           }
-          uint8_t* band = smem + K::OFF_BAND + bs * K::BAND_STAGE;
-          uint4* bz = reinterpret_cast<uint4*>(band);
-          for (int i = bt; i < K::BAND_STAGE / 16; i += 128) bz[i] = make_uint4(0, 0, 0, 0);
-          ptx::named_bar_sync(1, 128);
-          const uint32_t u0 = (uint32_t)kc * kBK;
-          for (uint32_t e = bt; e < E; e += 128) {
-            const uint32_t u = e % kBK;
-            const uint32_t lj = e / kBK;
-            const uint32_t j = lj % p.s;
-            const uint32_t ell = lj / p.s + 1;
-            const uint32_t g = gt[ell - 1];
-            const Draw dr = pattern(p, g, ell, u0 + u, j);
-            const uint32_t slot = (qmod + kappa - (ell % kappa)) % kappa;  // (q - ℓ) mod κ
-            const uint32_t rho = slot * p.B_r + dr.row;
-            const uint32_t m = rho >> 7, r7 = rho & 127;
-            const uint32_t off = m * kBandTile + (r7 >> 3) * 1024 + (r7 & 7) * 128 + (((u >> 3) ^ (r7 & 7)) << 4) +
-                                 (u & 7) * 2;
-            *reinterpret_cast<uint16_t*>(band + off) = dr.neg ? 0xBF80u : 0x3F80u;
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&acc_free[buf]);
+        }
+      }
+      // range end: outputs P+L-κ .. P+L-2 hold partial sums in S
+      for (int64_t i = P + L - (int64_t)kappa; i <= P + L - 2; ++i) {
+        const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
+#pragma unroll 1
+        for (int m = 0; m < NMT; ++m) {
+          const uint32_t base = m * 128 + qtr * 32;
+          if (base + 32 <= lo || base >= hi) continue;  // warp-uniform
+          const uint32_t rho = base + lane;
+          const bool in_slot = rho >= lo && rho < hi;
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t sv[16];
+            ptx::tmem_ld16(tmem_S + lane_off + m * BN + c0, sv);
+            ptx::tmem_wait_ld();
+            float tot[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) tot[t] = __uint_as_float(sv[t]);
+            if (in_slot) emit(i, m, rho, tot, c0);
+          }
+        }
+      }
+    } else if (warp >= 8 && warp < 16) {
+      // ===================== band generator =====================
+      const int bt = threadIdx.x - 256;
+      const uint32_t u = (uint32_t)bt & (kBK - 1);
+      const uint32_t cg = (uint32_t)bt >> 6;  // 0..3
+      const uint32_t ncombo = kappa * p.s;
+      const uint32_t band_u32 = ptx::smem_u32(smem + K::OFF_BAND);
+      const uint32_t ucol = u >> 3, ulo = (u & 7) * 2;
+      int bs = 0;
+      uint32_t bph = 0;
+      for (int64_t q = P; q < P + L; ++q) {
+        const int par = (int)(q & 1);
+        uint64_t* ck = ckey + par * kMaxCombos;
+        uint32_t* cr = crow + par * kMaxCombos;
+        for (int kc = 0; kc < nk; ++kc) {
+          ptx::mbar_wait(&band_empty[bs], bph ^ 1);
+          if (kc == 0) {
+            // per input block: hash key and band-row base for every (ℓ, j) combo
+            for (uint32_t c = bt; c < ncombo; c += K::NBANDT) {
+              const uint32_t ell = c / p.s + 1, j = c % p.s;
+              const int64_t iout = q - (int64_t)ell;  // output fed by this input block through π_ℓ
+              const uint32_t g = affine_pow(p, (uint64_t)mod_pos(iout, p.M), 0u);
+              ck[c] = (((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | (uint64_t)j) ^ p.K;
+              cr[c] = mod_pos(iout, kappa) * p.B_r + j * p.C;
+            }
+          }
+          uint4* bz = reinterpret_cast<uint4*>(smem + K::OFF_BAND + bs * K::BAND_STAGE);
+#pragma unroll
+          for (int i = 0; i < K::BAND_STAGE / 16 / K::NBANDT; ++i) bz[bt + i * K::NBANDT] = make_uint4(0, 0, 0, 0);
+          ptx::named_bar_sync(1, K::NBANDT);
+          const uint64_t uk = (uint64_t)((uint32_t)kc * kBK + u) << 8;
+          const uint32_t sbase = band_u32 + bs * K::BAND_STAGE;
+          for (uint32_t c = cg; c < ncombo; c += K::NBANDT / kBK) {
+            const uint64_t z = mix64(ck[c] ^ uk);
+            const uint32_t off = __umulhi((uint32_t)(z >> 32), p.C);  // R3
+            const uint32_t rho = cr[c] + off;
+            const uint32_t r7 = rho & 127;
+            const uint32_t addr = sbase + (rho >> 7) * kBandTile + (r7 >> 3) * 1024 + (r7 & 7) * 128 +
+                                  ((ucol ^ (r7 & 7)) << 4) + ulo;
+            ptx::st_shared_u16(addr, (z & 1) ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
           }
           ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&band_full[bs]);
           if (++bs == K::NBAND) bs = 0, bph ^= 1;
         }
       }
-    } else if (F32 && warp >= 12) {
+    } else if (F32 && warp >= 16) {
       // ===================== fp32 -> (hi, lo) bf16 split =====================
-      const int cv = threadIdx.x - 384;
+      const int cv = threadIdx.x - 512;
       int rs = 0, cs = 0;
       uint32_t rph = 0, cph = 0;
       const int64_t total = L * nk;
@@ -349,19 +402,17 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN>::NTHREADS, 1)
         uint8_t* lo = hi + K::CONV_HALF;
 #pragma unroll 4
         for (int idx = cv; idx < kBK * BN / 4; idx += 128) {
-          int rowk, c;  // (K index, MN index) of the first of 4 consecutive elements
           uint32_t off;
           if (!TRANS) {
-            rowk = idx / (BN / 4);
-            c = (idx % (BN / 4)) * 4;  // column
+            const int rowk = idx / (BN / 4);
+            const int c = (idx % (BN / 4)) * 4;  // column
             const int blk = c >> 6, cc = c & 63;
-            off = blk * (kBK * 128) + (rowk >> 3) * 1024 + (rowk & 7) * 128 + ((((cc >> 3) ^ (rowk & 7))) << 4) +
+            off = blk * (kBK * 128) + (rowk >> 3) * 1024 + (rowk & 7) * 128 + (((cc >> 3) ^ (rowk & 7)) << 4) +
                   (cc & 7) * 2;
           } else {
             const int v = idx / (kBK / 4);  // vector (MN)
-            c = (idx % (kBK / 4)) * 4;      // coordinate (K)
-            rowk = v;
-            off = (v >> 3) * 1024 + (v & 7) * 128 + ((((c >> 3) ^ (v & 7))) << 4) + (c & 7) * 2;
+            const int c = (idx % (kBK / 4)) * 4;      // coordinate (K)
+            off = (v >> 3) * 1024 + (v & 7) * 128 + (((c >> 3) ^ (v & 7)) << 4) + (c & 7) * 2;
           }
           const float4 a = *reinterpret_cast<const float4*>(raw + (size_t)idx * 4);
           const __nv_bfloat162 h01 = __floats2bfloat162_rn(a.x, a.y);
@@ -376,7 +427,6 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN>::NTHREADS, 1)
           lv.y = *reinterpret_cast<const uint32_t*>(&l23);
           *reinterpret_cast<uint2*>(hi + off) = hv;
           *reinterpret_cast<uint2*>(lo + off) = lv;
-          (void)rowk;
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&raw_empty[rs]);
@@ -415,7 +465,7 @@ EncodeTiledFn encode_fn() {
 
 struct Plan {
   bool ok = false;
-  int nmt = 1, bn = 128;
+  int nmt = 1;
   std::string why;
 };
 
@@ -435,18 +485,17 @@ Plan plan_for(const SketchParams& p, bps_dtype dt) {
     return pl;
   }
   pl.nmt = rows <= 128 ? 1 : 2;
-  pl.bn = (dt == BPS_BF16 && pl.nmt == 1) ? 256 : 128;
   pl.ok = true;
   return pl;
 }
 
-template <bool F32, bool TRANS, int NMT, int BN>
+template <bool F32, bool TRANS, int NMT>
 int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, float* Y, int64_t ldy,
                 const Placement& pl, cudaStream_t st) {
-  using K = Cfg<F32, TRANS, NMT, BN>;
+  using K = Cfg<F32, TRANS, NMT>;
+  constexpr int BN = K::BN;
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(BPS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
-  // geometry of the launch window
   TcArgs a;
   a.p = p;
   a.n = n;
@@ -465,6 +514,15 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     a.stream_len = p.M;
     in_rows = (int64_t)p.M * p.B_c;
   }
+  // accumulation group: largest divisor of B_c/64 that is <= 8 K-chunks (precision)
+  const int nk = (int)(p.B_c / kBK);
+  int G = 1;
+  for (int g = 8; g >= 1; --g)
+    if (nk % g == 0) {
+      G = g;
+      break;
+    }
+  a.G = G;
   const int64_t n_ct = (n + BN - 1) / BN;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -483,21 +541,18 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
   const CUtensorMapDataType tdt = F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   cuuint64_t dims[2], strides[1];
   cuuint32_t box[2], estr[2] = {1, 1};
-  CUtensorMapSwizzle swz;
+  const CUtensorMapSwizzle swz = F32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B;
+  strides[0] = (cuuint64_t)lda * K::ESZ;
   if (!TRANS) {
     dims[0] = (cuuint64_t)n;
     dims[1] = (cuuint64_t)in_rows;
-    strides[0] = (cuuint64_t)lda * K::ESZ;
     box[0] = F32 ? BN : 64;
     box[1] = kBK;
-    swz = F32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B;
   } else {
     dims[0] = (cuuint64_t)in_rows;  // coordinates (d)
     dims[1] = (cuuint64_t)n;        // vectors
-    strides[0] = (cuuint64_t)lda * K::ESZ;
     box[0] = kBK;
     box[1] = BN;
-    swz = F32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B;
   }
   CUresult cr = enc(&tm, tdt, 2, const_cast<void*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -505,11 +560,12 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
 
   // outputs split between two CTAs are accumulated with red.add into a zeroed Y
   if (p.kappa > 1) {
-    cudaError_t e = TRANS ? cudaMemset2DAsync(Y, ldy * 4, 0, (size_t)(pl.range_mode ? pl.n_out * p.B_r : (int64_t)p.M * p.B_r) * 4, n, st)
-                          : cudaMemset2DAsync(Y, ldy * 4, 0, (size_t)n * 4, (size_t)(pl.n_out * p.B_r), st);
+    const int64_t krows = pl.range_mode ? pl.n_out * (int64_t)p.B_r : (int64_t)p.M * p.B_r;
+    cudaError_t e = TRANS ? cudaMemset2DAsync(Y, ldy * 4, 0, (size_t)krows * 4, (size_t)n, st)
+                          : cudaMemset2DAsync(Y, ldy * 4, 0, (size_t)n * 4, (size_t)krows, st);
     if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaMemset2DAsync: ") + cudaGetErrorString(e));
   }
-  auto kern = bps_tc_kernel<F32, TRANS, NMT, BN>;
+  auto kern = bps_tc_kernel<F32, TRANS, NMT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
   if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
   kern<<<(unsigned)grid, K::NTHREADS, K::SMEM, st>>>(tm, a);
@@ -535,17 +591,17 @@ int launch_tc(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_
   Plan plan = plan_for(p, dt);
   if (!plan.ok) return fail(BPS_ERR_UNSUPPORTED, plan.why);
   const bool f32 = dt == BPS_F32;
-#define BPS_TC_CASE(F, T, NM, B)                                                 \
-  if (f32 == F && transposed == T && plan.nmt == NM && plan.bn == B)           \
-    return launch_impl<F, T, NM, B>(p, A, lda, n, Y, ldy, pl, st);
-  BPS_TC_CASE(true, false, 1, 128)
-  BPS_TC_CASE(true, false, 2, 128)
-  BPS_TC_CASE(true, true, 1, 128)
-  BPS_TC_CASE(true, true, 2, 128)
-  BPS_TC_CASE(false, false, 1, 256)
-  BPS_TC_CASE(false, false, 2, 128)
-  BPS_TC_CASE(false, true, 1, 256)
-  BPS_TC_CASE(false, true, 2, 128)
+#define BPS_TC_CASE(F, T, NM)                                 \
+  if (f32 == F && transposed == T && plan.nmt == NM)          \
+    return launch_impl<F, T, NM>(p, A, lda, n, Y, ldy, pl, st);
+  BPS_TC_CASE(true, false, 1)
+  BPS_TC_CASE(true, false, 2)
+  BPS_TC_CASE(true, true, 1)
+  BPS_TC_CASE(true, true, 2)
+  BPS_TC_CASE(false, false, 1)
+  BPS_TC_CASE(false, false, 2)
+  BPS_TC_CASE(false, true, 1)
+  BPS_TC_CASE(false, true, 2)
 #undef BPS_TC_CASE
   return fail(BPS_ERR_UNSUPPORTED, "no tc instantiation for this plan");
 }
