@@ -38,6 +38,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// waiting roles that are off the critical path back off so they do not steal issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
+}
 
 // ----------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {

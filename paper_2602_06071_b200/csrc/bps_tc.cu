@@ -35,37 +35,42 @@ namespace {
 
 constexpr int kBK = 64;                   // K rows per pipeline stage (one 128-byte swizzle row of bf16)
 constexpr int kBandTile = 128 * kBK * 2;  // one M-tile (128 band rows) of a band stage, bytes
-constexpr int kMaxCombos = 256;           // κ·s ≤ κ·B_r ≤ 256 on this path
+constexpr int kMaxGroup = 32;             // K-chunks per accumulation group (precision)
+constexpr int kCPT = 4;                   // (ℓ, j) combos per band thread kept in registers per pass
 
 // Warp roles: 0 TMA producer | 1 MMA issuer (+TMEM alloc) | 2-3 idle | 4-7 epilogue
 // (TMEM lane quarters 0-3) | 8-15 band generator | 16-19 fp32 hi/lo converter (fp32 only).
-template <bool F32, bool TRANS, int NMT>
+template <bool F32, bool TRANS, int NMT, int BN_>
 struct Cfg {
-  static constexpr int BN = 128 / NMT;  // data columns per CTA; TMEM = D0, D1, S each NMT·BN columns
+  static constexpr int BN = BN_;  // data columns per CTA; TMEM = D (NMT·BN) + S (NMT·BN)
   static constexpr int ESZ = F32 ? 4 : 2;
   static constexpr int RAW_STAGE = kBK * BN * ESZ;
-  static constexpr int NRAW = F32 ? (NMT == 1 ? 3 : 4) : (NMT == 1 ? 6 : 8);
   static constexpr int CONV_HALF = kBK * BN * 2;
   static constexpr int CONV_STAGE = F32 ? 2 * CONV_HALF : 0;
   static constexpr int NCONV = F32 ? 2 : 0;
   static constexpr int BAND_STAGE = NMT * kBandTile;
   static constexpr int NBAND = (NMT == 1 && !F32) ? 3 : 2;
+  static constexpr int BUDGET = 210 * 1024;
+  static constexpr int NRAW_FIT = (BUDGET - NCONV * CONV_STAGE - NBAND * BAND_STAGE) / RAW_STAGE;
+  static constexpr int NRAW = NRAW_FIT > 8 ? 8 : NRAW_FIT;
   static constexpr int OFF_RAW = 0;
   static constexpr int OFF_CONV = OFF_RAW + NRAW * RAW_STAGE;
   static constexpr int OFF_BAND = OFF_CONV + NCONV * CONV_STAGE;
-  static constexpr int OFF_CKEY = OFF_BAND + NBAND * BAND_STAGE;   // [2][kMaxCombos] u64
-  static constexpr int OFF_CROW = OFF_CKEY + 2 * kMaxCombos * 8;   // [2][kMaxCombos] u32
-  static constexpr int OFF_BAR = OFF_CROW + 2 * kMaxCombos * 4;
-  // raw full/empty, conv full/empty, band full/empty, acc full[2], acc free[2]
-  static constexpr int NBARS = 2 * NRAW + 2 * NCONV + 2 * NBAND + 4;
+  static constexpr int OFF_CKEY = OFF_BAND + NBAND * BAND_STAGE;  // [2][256] u64 per-block combo keys
+  static constexpr int OFF_CROW = OFF_CKEY + 2 * 256 * 8;          // [2][256] u32 per-block band-row bases
+  static constexpr int OFF_BAR = OFF_CROW + 2 * 256 * 4;
+  // raw full/empty, conv full/empty, band full/empty, acc full, acc free
+  static constexpr int NBARS = 2 * NRAW + 2 * NCONV + 2 * NBAND + 2;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBARS * 8;
   static constexpr int SMEM = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
   static constexpr int NWARPS = F32 ? 20 : 16;
   static constexpr int NTHREADS = NWARPS * 32;
   static constexpr int NBANDT = 256;  // band generator threads
-  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr uint32_t TMEM_COLS = (2 * NMT * BN <= 256) ? 256 : 512;
   static constexpr uint32_t IDESC = ptx::idesc_bf16(128, BN, !TRANS);
-  static_assert(3 * NMT * BN <= 512, "TMEM");
+  static_assert(NRAW >= 2, "smem: raw ring");
+  static_assert(2 * NMT * BN <= 512, "TMEM");
+  static_assert(BN % 64 == 0 && BN <= 256, "BN");
   static_assert(SMEM <= 227 * 1024, "smem");
 };
 
@@ -87,10 +92,10 @@ __device__ __forceinline__ uint32_t mod_pos(int64_t i, uint32_t M) {
   return (uint32_t)(r < 0 ? r + M : r);
 }
 
-template <bool F32, bool TRANS, int NMT>
-__global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
+template <bool F32, bool TRANS, int NMT, int BN_>
+__global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
     bps_tc_kernel(const __grid_constant__ CUtensorMap tmap, const TcArgs args) {
-  using K = Cfg<F32, TRANS, NMT>;
+  using K = Cfg<F32, TRANS, NMT, BN_>;
   constexpr int BN = K::BN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -101,11 +106,11 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
   uint64_t* conv_empty = conv_full + K::NCONV;
   uint64_t* band_full = conv_empty + K::NCONV;
   uint64_t* band_empty = band_full + K::NBAND;
-  uint64_t* acc_full = band_empty + K::NBAND;  // [2]
-  uint64_t* acc_free = acc_full + 2;           // [2]
+  uint64_t* acc_full = band_empty + K::NBAND;
+  uint64_t* acc_free = acc_full + 1;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + K::OFF_TMEMPTR);
   uint64_t* ckey = reinterpret_cast<uint64_t*>(smem + K::OFF_CKEY);
   uint32_t* crow = reinterpret_cast<uint32_t*>(smem + K::OFF_CROW);
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + K::OFF_TMEMPTR);
 
   const SketchParams& p = args.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -133,10 +138,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
       ptx::mbar_init(&band_full[i], K::NBANDT);
       ptx::mbar_init(&band_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&acc_full[i], 1);
-      ptx::mbar_init(&acc_free[i], 128);
-    }
+    ptx::mbar_init(acc_full, 1);
+    ptx::mbar_init(acc_free, 128);
     ptx::fence_mbar_init();
     ptx::tma_prefetch(&tmap);
   }
@@ -144,8 +147,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_ptr;
-  const uint32_t tmem_S = tmem + 2 * NMT * BN;  // fp32 running sums (RN adds on CUDA cores)
+  const uint32_t tmem = *tmem_ptr;               // D: per-group tensor-core accumulator
+  const uint32_t tmem_S = tmem + NMT * BN;       // S: fp32 running sums (RN adds on CUDA cores)
 
   if (L > 0) {
     if (warp == 0) {
@@ -158,7 +161,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
         for (int64_t q = P; q < P + L; ++q) {
           const int64_t row0 = args.range_mode ? (q - (args.pos_begin + 1)) * (int64_t)p.B_c : (int64_t)gq * p.B_c;
           for (int kc = 0; kc < nk; ++kc) {
-            ptx::mbar_wait(&raw_empty[s], ph ^ 1);
+            ptx::mbar_wait_sleep(&raw_empty[s], ph ^ 1, 20);
             ptx::mbar_arrive_expect_tx(&raw_full[s], K::RAW_STAGE);
             uint8_t* dst = smem + K::OFF_RAW + s * K::RAW_STAGE;
             const int32_t r = (int32_t)(row0 + kc * kBK);
@@ -182,22 +185,20 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
       // ===================== MMA issuer =====================
       if (lane == 0) {
         int ds = 0, bs = 0;
-        uint32_t dph = 0, bph = 0;
-        uint32_t fbits = 0;  // phase bit per accumulator buffer
-        uint32_t grp = 0;
+        uint32_t dph = 0, bph = 0, fph = 0;
         uint64_t* dfull = F32 ? conv_full : raw_full;
         uint64_t* dempty = F32 ? conv_empty : raw_empty;
         constexpr int NDS = F32 ? K::NCONV : K::NRAW;
         const uint32_t data_base = ptx::smem_u32(smem + (F32 ? K::OFF_CONV : K::OFF_RAW));
         constexpr int DSTAGE = F32 ? K::CONV_STAGE : K::RAW_STAGE;
         const uint32_t band_base = ptx::smem_u32(smem + K::OFF_BAND);
+        bool first_group = true;
         for (int64_t q = P; q < P + L; ++q) {
           for (int kc = 0; kc < nk; ++kc) {
             const int gi = kc % G;
-            const uint32_t buf = grp & 1;
-            if (gi == 0 && grp >= 2) {  // accumulator buffer must have been flushed into S
-              ptx::mbar_wait(&acc_free[buf], (fbits >> buf) & 1u);
-              fbits ^= 1u << buf;
+            if (gi == 0 && !first_group) {  // D must have been folded into S
+              ptx::mbar_wait(acc_free, fph);
+              fph ^= 1;
               ptx::tc_fence_after();
             }
             ptx::mbar_wait(&dfull[ds], dph);
@@ -205,7 +206,6 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
             ptx::tc_fence_after();
             const uint32_t dbase = data_base + ds * DSTAGE;
             const uint32_t bbase = band_base + bs * K::BAND_STAGE;
-            const uint32_t dacc = tmem + buf * (NMT * BN);
 #pragma unroll
             for (int ks = 0; ks < kBK / 16; ++ks) {
 #pragma unroll
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
                   const uint64_t bdesc = TRANS ? ptx::smem_desc_sw128(pb + ks * 32, 0, 1024)
                                                : ptx::smem_desc_sw128(pb + ks * 16 * 128, kBK * 128, 1024);
                   const uint32_t acc = (gi == 0 && ks == 0 && part == 0) ? 0u : 1u;  // fresh per group
-                  ptx::mma_bf16_ss(dacc + m * BN, adesc, bdesc, K::IDESC, acc);
+                  ptx::mma_bf16_ss(tmem + m * BN, adesc, bdesc, K::IDESC, acc);
                 }
               }
             }
@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
             if (++ds == NDS) ds = 0, dph ^= 1;
             if (++bs == K::NBAND) bs = 0, bph ^= 1;
             if (gi == G - 1) {
-              ptx::mma_commit(&acc_full[buf]);
-              ++grp;
+              ptx::mma_commit(acc_full);
+              first_group = false;
             }
           }
         }
@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
         for (int c = 0; c < NMT * BN; c += 16) ptx::tmem_st16(tmem_S + lane_off + c, z);
         ptx::tmem_wait_st();
       }
-      auto emit = [&](int64_t i, int m, uint32_t rho, const float* vals, int c0) {
-        // vals: 16 S values of output row (rho - slot lo) of output i, columns col0+c0..+15
+      auto emit = [&](int64_t i, uint32_t rho, const float* vals, int c0) {
+        // vals: 16 sums of band row rho (slot of output i), columns col0+c0 .. +15
         const bool owned = args.range_mode ? (i >= args.pos_begin && i < args.pos_end) : true;
         if (!owned) return;
         const uint32_t lo = mod_pos(i, kappa) * p.B_r;
@@ -253,7 +253,6 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
                                              : (int64_t)affine_pow(p, (uint64_t)mod_pos(i, p.M), 0u) * p.B_r) +
                             (int64_t)(rho - lo);
         const int64_t cbase = col0 + c0;
-        (void)m;
         if (!TRANS) {
           float* y = args.Y + row * args.ldy + cbase;
 #pragma unroll
@@ -284,33 +283,30 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
           }
         }
       };
-      uint32_t abits = 0;  // phase bit per accumulator buffer
-      uint32_t grp = 0;
+      uint32_t aph = 0;
       const int ngrp = nk / G;
       for (int64_t q = P; q < P + L; ++q) {
-        for (int gix = 0; gix < ngrp; ++gix, ++grp) {
-          const uint32_t buf = grp & 1;
-          ptx::mbar_wait(&acc_full[buf], (abits >> buf) & 1u);
-          abits ^= 1u << buf;
+        const int64_t i = q - (int64_t)kappa;  // output completed by input block q
+        const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
+        for (int gix = 0; gix < ngrp; ++gix) {
+          ptx::mbar_wait_sleep(acc_full, aph, 32);
+          aph ^= 1;
           ptx::tc_fence_after();
           const bool last = gix == ngrp - 1;
-          const int64_t i = q - (int64_t)kappa;  // output completed by input block q
-          const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
 #pragma unroll 1
           for (int m = 0; m < NMT; ++m) {
             const uint32_t rho = m * 128 + qtr * 32 + lane;
-            const bool quarter_hit = last && !(m * 128 + qtr * 32 + 32 <= lo || m * 128 + qtr * 32 >= hi);
             const bool in_slot = last && rho >= lo && rho < hi;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 16) {
               uint32_t d[16], sv[16];
-              ptx::tmem_ld16(tmem + buf * (NMT * BN) + lane_off + m * BN + c0, d);
+              ptx::tmem_ld16(tmem + lane_off + m * BN + c0, d);
               ptx::tmem_ld16(tmem_S + lane_off + m * BN + c0, sv);
               ptx::tmem_wait_ld();
               float tot[16];
 #pragma unroll
               for (int t = 0; t < 16; ++t) tot[t] = __uint_as_float(sv[t]) + __uint_as_float(d[t]);
-              if (quarter_hit && in_slot) emit(i, m, rho, tot, c0);
+              if (in_slot) emit(i, rho, tot, c0);
 #pragma unroll
               for (int t = 0; t < 16; ++t) sv[t] = in_slot ? 0u : __float_as_uint(tot[t]);
               ptx::tmem_st16(tmem_S + lane_off + m * BN + c0, sv);
@@ -318,7 +314,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
           }
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
-          ptx::mbar_arrive(&acc_free[buf]);
+          ptx::mbar_arrive(acc_free);
         }
       }
       // range end: outputs P+L-κ .. P+L-2 hold partial sums in S
@@ -338,12 +334,13 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
             float tot[16];
 #pragma unroll
             for (int t = 0; t < 16; ++t) tot[t] = __uint_as_float(sv[t]);
-            if (in_slot) emit(i, m, rho, tot, c0);
+            if (in_slot) emit(i, rho, tot, c0);
           }
         }
       }
     } else if (warp >= 8 && warp < 16) {
       // ===================== band generator =====================
+      // Thread (u, cg): column u of every band stage, combos c = cg, cg+4, ... (c = (ℓ-1)·s + j).
       const int bt = threadIdx.x - 256;
       const uint32_t u = (uint32_t)bt & (kBK - 1);
       const uint32_t cg = (uint32_t)bt >> 6;  // 0..3
@@ -353,16 +350,16 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
       int bs = 0;
       uint32_t bph = 0;
       for (int64_t q = P; q < P + L; ++q) {
-        const int par = (int)(q & 1);
-        uint64_t* ck = ckey + par * kMaxCombos;
-        uint32_t* cr = crow + par * kMaxCombos;
+        const int par = (int)(q & 1);  // tables double-buffered by block parity
+        uint64_t* ck = ckey + par * 256;
+        uint32_t* cr = crow + par * 256;
         for (int kc = 0; kc < nk; ++kc) {
           ptx::mbar_wait(&band_empty[bs], bph ^ 1);
           if (kc == 0) {
-            // per input block: hash key and band-row base for every (ℓ, j) combo
+            // per input block q: hash key and band-row base of every combo (ℓ, j) — output q-ℓ
             for (uint32_t c = bt; c < ncombo; c += K::NBANDT) {
               const uint32_t ell = c / p.s + 1, j = c % p.s;
-              const int64_t iout = q - (int64_t)ell;  // output fed by this input block through π_ℓ
+              const int64_t iout = q - (int64_t)ell;
               const uint32_t g = affine_pow(p, (uint64_t)mod_pos(iout, p.M), 0u);
               ck[c] = (((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | (uint64_t)j) ^ p.K;
               cr[c] = mod_pos(iout, kappa) * p.B_r + j * p.C;
@@ -374,14 +371,25 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
           ptx::named_bar_sync(1, K::NBANDT);
           const uint64_t uk = (uint64_t)((uint32_t)kc * kBK + u) << 8;
           const uint32_t sbase = band_u32 + bs * K::BAND_STAGE;
-          for (uint32_t c = cg; c < ncombo; c += K::NBANDT / kBK) {
-            const uint64_t z = mix64(ck[c] ^ uk);
-            const uint32_t off = __umulhi((uint32_t)(z >> 32), p.C);  // R3
-            const uint32_t rho = cr[c] + off;
-            const uint32_t r7 = rho & 127;
-            const uint32_t addr = sbase + (rho >> 7) * kBandTile + (r7 >> 3) * 1024 + (r7 & 7) * 128 +
-                                  ((ucol ^ (r7 & 7)) << 4) + ulo;
-            ptx::st_shared_u16(addr, (z & 1) ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
+          for (uint32_t c0 = cg; c0 < ncombo; c0 += 4 * kCPT) {
+            uint64_t z[kCPT];
+            uint32_t rb[kCPT];
+#pragma unroll
+            for (int t = 0; t < kCPT; ++t) {
+              const uint32_t c = c0 + 4 * t;
+              const uint32_t cc = c < ncombo ? c : c0;
+              z[t] = mix64(ck[cc] ^ uk);
+              rb[t] = cr[cc];
+            }
+#pragma unroll
+            for (int t = 0; t < kCPT; ++t) {
+              if (c0 + 4 * t >= ncombo) continue;
+              const uint32_t rho = rb[t] + __umulhi((uint32_t)(z[t] >> 32), p.C);  // R3
+              const uint32_t r7 = rho & 127;
+              const uint32_t addr = sbase + (rho >> 7) * kBandTile + (r7 >> 3) * 1024 + (r7 & 7) * 128 +
+                                    ((ucol ^ (r7 & 7)) << 4) + ulo;
+              ptx::st_shared_u16(addr, (z[t] & 1) ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
+            }
           }
           ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&band_full[bs]);
@@ -410,8 +418,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT>::NTHREADS, 1)
             off = blk * (kBK * 128) + (rowk >> 3) * 1024 + (rowk & 7) * 128 + (((cc >> 3) ^ (rowk & 7)) << 4) +
                   (cc & 7) * 2;
           } else {
-            const int v = idx / (kBK / 4);  // vector (MN)
-            const int c = (idx % (kBK / 4)) * 4;      // coordinate (K)
+            const int v = idx / (kBK / 4);        // vector (MN)
+            const int c = (idx % (kBK / 4)) * 4;  // coordinate (K)
             off = (v >> 3) * 1024 + (v & 7) * 128 + (((c >> 3) ^ (v & 7)) << 4) + (c & 7) * 2;
           }
           const float4 a = *reinterpret_cast<const float4*>(raw + (size_t)idx * 4);
@@ -466,6 +474,7 @@ EncodeTiledFn encode_fn() {
 struct Plan {
   bool ok = false;
   int nmt = 1;
+  int bn = 128;
   std::string why;
 };
 
@@ -489,10 +498,20 @@ Plan plan_for(const SketchParams& p, bps_dtype dt) {
   return pl;
 }
 
-template <bool F32, bool TRANS, int NMT>
+// ranges per column tile: as many as fill the SMs, each ≥ κ-1 input blocks long so that
+// every split output has exactly two contributors (deterministic red.add, see header)
+int64_t ranges_for(const SketchParams& p, int64_t stream_len, int64_t n_ct, int sms) {
+  int64_t R = n_ct >= sms ? 1 : sms / n_ct;
+  if (R > stream_len) R = stream_len;
+  const int64_t need = p.kappa > 1 ? (int64_t)p.kappa - 1 : 1;
+  while (R > 1 && stream_len / R < need) --R;
+  return R;
+}
+
+template <bool F32, bool TRANS, int NMT, int BN_>
 int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, float* Y, int64_t ldy,
                 const Placement& pl, cudaStream_t st) {
-  using K = Cfg<F32, TRANS, NMT>;
+  using K = Cfg<F32, TRANS, NMT, BN_>;
   constexpr int BN = K::BN;
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(BPS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
@@ -514,10 +533,10 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     a.stream_len = p.M;
     in_rows = (int64_t)p.M * p.B_c;
   }
-  // accumulation group: largest divisor of B_c/64 that is <= 8 K-chunks (precision)
+  // accumulation group: largest divisor of B_c/64 that is <= kMaxGroup K-chunks (precision)
   const int nk = (int)(p.B_c / kBK);
   int G = 1;
-  for (int g = 8; g >= 1; --g)
+  for (int g = kMaxGroup; g >= 1; --g)
     if (nk % g == 0) {
       G = g;
       break;
@@ -527,10 +546,7 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t R = n_ct >= sms ? 1 : sms / n_ct;
-  if (R > a.stream_len) R = a.stream_len;
-  const int64_t need = p.kappa > 1 ? (int64_t)p.kappa - 1 : 1;
-  while (R > 1 && a.stream_len / R < need) --R;  // ≤ 2 contributors per split output
+  const int64_t R = ranges_for(p, a.stream_len, n_ct, sms);
   a.R = (int)R;
   const int64_t grid = n_ct * R;
   if (grid > 0x7FFFFFFF) return fail(BPS_ERR_UNSUPPORTED, "grid too large");
@@ -565,7 +581,7 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
                           : cudaMemset2DAsync(Y, ldy * 4, 0, (size_t)n * 4, (size_t)krows, st);
     if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaMemset2DAsync: ") + cudaGetErrorString(e));
   }
-  auto kern = bps_tc_kernel<F32, TRANS, NMT>;
+  auto kern = bps_tc_kernel<F32, TRANS, NMT, BN_>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
   if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
   kern<<<(unsigned)grid, K::NTHREADS, K::SMEM, st>>>(tm, a);
@@ -591,17 +607,33 @@ int launch_tc(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_
   Plan plan = plan_for(p, dt);
   if (!plan.ok) return fail(BPS_ERR_UNSUPPORTED, plan.why);
   const bool f32 = dt == BPS_F32;
-#define BPS_TC_CASE(F, T, NM)                                 \
-  if (f32 == F && transposed == T && plan.nmt == NM)          \
-    return launch_impl<F, T, NM>(p, A, lda, n, Y, ldy, pl, st);
-  BPS_TC_CASE(true, false, 1)
-  BPS_TC_CASE(true, false, 2)
-  BPS_TC_CASE(true, true, 1)
-  BPS_TC_CASE(true, true, 2)
-  BPS_TC_CASE(false, false, 1)
-  BPS_TC_CASE(false, false, 2)
-  BPS_TC_CASE(false, true, 1)
-  BPS_TC_CASE(false, true, 2)
+  // bf16, one M-tile: 256 columns per CTA (band reused over twice the columns) unless that
+  // leaves SMs idle, then 128.
+  int bn = 128;
+  if (!f32 && plan.nmt == 1) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t sl = pl.range_mode ? pl.n_out + p.kappa - 1 : (int64_t)p.M;
+    const int64_t ct256 = (n + 255) / 256, ct128 = (n + 127) / 128;
+    const int64_t used256 = ct256 * ranges_for(p, sl, ct256, sms);
+    const int64_t used128 = ct128 * ranges_for(p, sl, ct128, sms);
+    bn = (used256 * 10 >= used128 * 9 || used256 >= sms) ? 256 : 128;
+  }
+#define BPS_TC_CASE(F, T, NM, B)                                        \
+  if (f32 == F && transposed == T && plan.nmt == NM && bn == B)         \
+    return launch_impl<F, T, NM, B>(p, A, lda, n, Y, ldy, pl, st);
+  BPS_TC_CASE(true, false, 1, 128)
+  BPS_TC_CASE(true, true, 1, 128)
+  if (f32) bn = 64;
+  BPS_TC_CASE(true, false, 2, 64)
+  BPS_TC_CASE(true, true, 2, 64)
+  BPS_TC_CASE(false, false, 1, 256)
+  BPS_TC_CASE(false, true, 1, 256)
+  BPS_TC_CASE(false, false, 1, 128)
+  BPS_TC_CASE(false, true, 1, 128)
+  BPS_TC_CASE(false, false, 2, 128)
+  BPS_TC_CASE(false, true, 2, 128)
 #undef BPS_TC_CASE
   return fail(BPS_ERR_UNSUPPORTED, "no tc instantiation for this plan");
 }
