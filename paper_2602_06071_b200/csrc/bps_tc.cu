@@ -398,43 +398,59 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
       }
     } else if (F32 && warp >= 16) {
       // ===================== fp32 -> (hi, lo) bf16 split =====================
+      // a = hi + lo, hi = bf16_rn(a), lo = bf16_rn(a - hi): |a - hi - lo| ≤ 2^-17 |a|.
+      // Thread cv owns 4 consecutive MN (or K) elements of rows cv/(BN/4) + RPI·i; the
+      // swizzled destination offset is affine in i, so it is precomputed (two parities).
       const int cv = threadIdx.x - 512;
+      constexpr int NIT = kBK * BN / 4 / 128;  // float4 per thread per stage
+      uint32_t off_even, off_odd;
+      if (!TRANS) {
+        constexpr int F4R = BN / 4;            // float4 per data row
+        constexpr int RPI = 128 / F4R;         // rows advanced per iteration (4 or 8)
+        const int rowk0 = cv / F4R, c = (cv % F4R) * 4;
+        const int blk = c >> 6, cc = c & 63;
+        auto offr = [&](int rk) {
+          return (uint32_t)(blk * (kBK * 128) + (rk >> 3) * 1024 + (rk & 7) * 128 + (((cc >> 3) ^ (rk & 7)) << 4) +
+                            (cc & 7) * 2);
+        };
+        off_even = offr(rowk0);
+        off_odd = offr(rowk0 + RPI);  // used when RPI == 4 (rows of odd iterations have (row & 7) + 4)
+      } else {
+        const int v0 = cv / (kBK / 4), c = (cv % (kBK / 4)) * 4;  // vector, coordinate
+        off_even = (uint32_t)((v0 >> 3) * 1024 + (v0 & 7) * 128 + (((c >> 3) ^ (v0 & 7)) << 4) + (c & 7) * 2);
+        off_odd = off_even;  // v advances by 8 per iteration: same (v & 7)
+      }
       int rs = 0, cs = 0;
       uint32_t rph = 0, cph = 0;
       const int64_t total = L * nk;
+      const uint32_t raw_u32 = ptx::smem_u32(smem + K::OFF_RAW);
+      const uint32_t conv_u32 = ptx::smem_u32(smem + K::OFF_CONV);
       for (int64_t it = 0; it < total; ++it) {
         ptx::mbar_wait(&raw_full[rs], rph);
         ptx::mbar_wait(&conv_empty[cs], cph ^ 1);
-        const float* raw = reinterpret_cast<const float*>(smem + K::OFF_RAW + rs * K::RAW_STAGE);
-        uint8_t* hi = smem + K::OFF_CONV + cs * K::CONV_STAGE;
-        uint8_t* lo = hi + K::CONV_HALF;
-#pragma unroll 4
-        for (int idx = cv; idx < kBK * BN / 4; idx += 128) {
+        const uint32_t rbase = raw_u32 + rs * K::RAW_STAGE + cv * 16;
+        const uint32_t hbase = conv_u32 + cs * K::CONV_STAGE;
+#pragma unroll
+        for (int i = 0; i < NIT; ++i) {
           uint32_t off;
-          if (!TRANS) {
-            const int rowk = idx / (BN / 4);
-            const int c = (idx % (BN / 4)) * 4;  // column
-            const int blk = c >> 6, cc = c & 63;
-            off = blk * (kBK * 128) + (rowk >> 3) * 1024 + (rowk & 7) * 128 + (((cc >> 3) ^ (rowk & 7)) << 4) +
-                  (cc & 7) * 2;
-          } else {
-            const int v = idx / (kBK / 4);        // vector (MN)
-            const int c = (idx % (kBK / 4)) * 4;  // coordinate (K)
-            off = (v >> 3) * 1024 + (v & 7) * 128 + (((c >> 3) ^ (v & 7)) << 4) + (c & 7) * 2;
-          }
-          const float4 a = *reinterpret_cast<const float4*>(raw + (size_t)idx * 4);
-          const __nv_bfloat162 h01 = __floats2bfloat162_rn(a.x, a.y);
-          const __nv_bfloat162 h23 = __floats2bfloat162_rn(a.z, a.w);
-          const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
-          const __nv_bfloat162 l01 = __floats2bfloat162_rn(a.x - f01.x, a.y - f01.y);
-          const __nv_bfloat162 l23 = __floats2bfloat162_rn(a.z - f23.x, a.w - f23.y);
-          uint2 hv, lv;
-          hv.x = *reinterpret_cast<const uint32_t*>(&h01);
-          hv.y = *reinterpret_cast<const uint32_t*>(&h23);
-          lv.x = *reinterpret_cast<const uint32_t*>(&l01);
-          lv.y = *reinterpret_cast<const uint32_t*>(&l23);
-          *reinterpret_cast<uint2*>(hi + off) = hv;
-          *reinterpret_cast<uint2*>(lo + off) = lv;
+          if (!TRANS && (128 / (BN / 4)) == 4)
+            off = ((i & 1) ? off_odd : off_even) + (uint32_t)(i >> 1) * 1024u;  // 8 rows per 2 iterations
+          else
+            off = off_even + (uint32_t)i * 1024u;  // 8 rows (or vectors) per iteration
+          float4 a;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w)
+                       : "r"(rbase + i * 2048));
+          uint32_t h01, h23, l01, l23;
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(a.y), "f"(a.x));
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h23) : "f"(a.w), "f"(a.z));
+          const float r0 = a.x - __uint_as_float(h01 << 16), r1 = a.y - __uint_as_float(h01 & 0xFFFF0000u);
+          const float r2 = a.z - __uint_as_float(h23 << 16), r3 = a.w - __uint_as_float(h23 & 0xFFFF0000u);
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l01) : "f"(r1), "f"(r0));
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l23) : "f"(r3), "f"(r2));
+          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(hbase + off), "r"(h01), "r"(h23) : "memory");
+          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(hbase + K::CONV_HALF + off), "r"(l01), "r"(l23)
+                       : "memory");
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&raw_empty[rs]);
