@@ -39,7 +39,7 @@ constexpr int kMaxGroup = 32;             // K-chunks per accumulation group (pr
 constexpr int kCPT = 4;                   // (ℓ, j) combos per band thread kept in registers per pass
 
 // Warp roles: 0 TMA producer | 1 MMA issuer (+TMEM alloc) | 2-3 idle | 4-7 epilogue
-// (TMEM lane quarters 0-3) | 8-15 band generator | 16-19 fp32 hi/lo converter (fp32 only).
+// (TMEM lane quarters 0-3) | 8-15 band generator | 16-23 fp32 hi/lo converter (fp32 only).
 template <bool F32, bool TRANS, int NMT, int BN_>
 struct Cfg {
   static constexpr int BN = BN_;  // data columns per CTA; TMEM = D (NMT·BN) + S (NMT·BN)
@@ -47,7 +47,7 @@ struct Cfg {
   static constexpr int RAW_STAGE = kBK * BN * ESZ;
   static constexpr int CONV_HALF = kBK * BN * 2;
   static constexpr int CONV_STAGE = F32 ? 2 * CONV_HALF : 0;
-  static constexpr int NCONV = F32 ? 2 : 0;
+  static constexpr int NCONV = F32 ? 3 : 0;
   static constexpr int BAND_STAGE = NMT * kBandTile;
   static constexpr int NBAND = (NMT == 1 && !F32) ? 3 : 2;
   static constexpr int BUDGET = 210 * 1024;
@@ -63,7 +63,8 @@ struct Cfg {
   static constexpr int NBARS = 2 * NRAW + 2 * NCONV + 2 * NBAND + 2;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBARS * 8;
   static constexpr int SMEM = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
-  static constexpr int NWARPS = F32 ? 20 : 16;
+  static constexpr int NWARPS = F32 ? 24 : 16;
+  static constexpr int NCONVT = 256;  // fp32 converter threads (warps 16-23)
   static constexpr int NTHREADS = NWARPS * 32;
   static constexpr int NBANDT = 256;  // band generator threads
   static constexpr uint32_t TMEM_COLS = (2 * NMT * BN <= 256) ? 256 : 512;
@@ -128,10 +129,10 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < K::NRAW; ++i) {
       ptx::mbar_init(&raw_full[i], 1);
-      ptx::mbar_init(&raw_empty[i], F32 ? 128 : 1);
+      ptx::mbar_init(&raw_empty[i], F32 ? K::NCONVT : 1);
     }
     for (int i = 0; i < K::NCONV; ++i) {
-      ptx::mbar_init(&conv_full[i], 128);
+      ptx::mbar_init(&conv_full[i], K::NCONVT);
       ptx::mbar_init(&conv_empty[i], 1);
     }
     for (int i = 0; i < K::NBAND; ++i) {
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         uint64_t* ck = ckey + par * 256;
         uint32_t* cr = crow + par * 256;
         for (int kc = 0; kc < nk; ++kc) {
-          ptx::mbar_wait(&band_empty[bs], bph ^ 1);
+          ptx::mbar_wait_sleep(&band_empty[bs], bph ^ 1, 20);
           if (kc == 0) {
             // per input block q: hash key and band-row base of every combo (ℓ, j) — output q-ℓ
             for (uint32_t c = bt; c < ncombo; c += K::NBANDT) {
@@ -402,11 +403,14 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
       // Thread cv owns 4 consecutive MN (or K) elements of rows cv/(BN/4) + RPI·i; the
       // swizzled destination offset is affine in i, so it is precomputed (two parities).
       const int cv = threadIdx.x - 512;
-      constexpr int NIT = kBK * BN / 4 / 128;  // float4 per thread per stage
-      uint32_t off_even, off_odd;
+      constexpr int NT = K::NCONVT;
+      constexpr int NIT = kBK * BN / 4 / NT;  // float4 per thread per stage
+      static_assert(NIT * NT * 4 == kBK * BN, "converter tiling");
+      // destination byte offset of iteration i = off_base[i & 1] + (i >> 1)·dstep (+ i·istep)
+      uint32_t off_even, off_odd, istep;
       if (!TRANS) {
-        constexpr int F4R = BN / 4;            // float4 per data row
-        constexpr int RPI = 128 / F4R;         // rows advanced per iteration (4 or 8)
+        constexpr int F4R = BN / 4;     // float4 per data row
+        constexpr int RPI = NT / F4R;   // rows advanced per iteration (8 for BN=128, 16 for BN=64)
         const int rowk0 = cv / F4R, c = (cv % F4R) * 4;
         const int blk = c >> 6, cc = c & 63;
         auto offr = [&](int rk) {
@@ -414,43 +418,38 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
                             (cc & 7) * 2);
         };
         off_even = offr(rowk0);
-        off_odd = offr(rowk0 + RPI);  // used when RPI == 4 (rows of odd iterations have (row & 7) + 4)
+        off_odd = off_even;
+        istep = (uint32_t)(RPI / 8) * 1024u;  // RPI is a multiple of 8: (row & 7) is invariant
       } else {
-        const int v0 = cv / (kBK / 4), c = (cv % (kBK / 4)) * 4;  // vector, coordinate
+        constexpr int RPI = NT / (kBK / 4);  // vectors advanced per iteration (16)
+        const int v0 = cv / (kBK / 4), c = (cv % (kBK / 4)) * 4;
         off_even = (uint32_t)((v0 >> 3) * 1024 + (v0 & 7) * 128 + (((c >> 3) ^ (v0 & 7)) << 4) + (c & 7) * 2);
-        off_odd = off_even;  // v advances by 8 per iteration: same (v & 7)
+        off_odd = off_even;
+        istep = (uint32_t)(RPI / 8) * 1024u;
       }
+      (void)off_odd;
       int rs = 0, cs = 0;
       uint32_t rph = 0, cph = 0;
       const int64_t total = L * nk;
-      const uint32_t raw_u32 = ptx::smem_u32(smem + K::OFF_RAW);
-      const uint32_t conv_u32 = ptx::smem_u32(smem + K::OFF_CONV);
       for (int64_t it = 0; it < total; ++it) {
         ptx::mbar_wait(&raw_full[rs], rph);
         ptx::mbar_wait(&conv_empty[cs], cph ^ 1);
-        const uint32_t rbase = raw_u32 + rs * K::RAW_STAGE + cv * 16;
-        const uint32_t hbase = conv_u32 + cs * K::CONV_STAGE;
+        const float4* rawp = reinterpret_cast<const float4*>(smem + K::OFF_RAW + rs * K::RAW_STAGE) + cv;
+        uint8_t* hbase = smem + K::OFF_CONV + cs * K::CONV_STAGE + off_even;
+        float4 a[NIT];
+#pragma unroll
+        for (int i = 0; i < NIT; ++i) a[i] = rawp[i * NT];
 #pragma unroll
         for (int i = 0; i < NIT; ++i) {
-          uint32_t off;
-          if (!TRANS && (128 / (BN / 4)) == 4)
-            off = ((i & 1) ? off_odd : off_even) + (uint32_t)(i >> 1) * 1024u;  // 8 rows per 2 iterations
-          else
-            off = off_even + (uint32_t)i * 1024u;  // 8 rows (or vectors) per iteration
-          float4 a;
-          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                       : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w)
-                       : "r"(rbase + i * 2048));
           uint32_t h01, h23, l01, l23;
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(a.y), "f"(a.x));
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h23) : "f"(a.w), "f"(a.z));
-          const float r0 = a.x - __uint_as_float(h01 << 16), r1 = a.y - __uint_as_float(h01 & 0xFFFF0000u);
-          const float r2 = a.z - __uint_as_float(h23 << 16), r3 = a.w - __uint_as_float(h23 & 0xFFFF0000u);
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(a[i].y), "f"(a[i].x));
+          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h23) : "f"(a[i].w), "f"(a[i].z));
+          const float r0 = a[i].x - __uint_as_float(h01 << 16), r1 = a[i].y - __uint_as_float(h01 & 0xFFFF0000u);
+          const float r2 = a[i].z - __uint_as_float(h23 << 16), r3 = a[i].w - __uint_as_float(h23 & 0xFFFF0000u);
           asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l01) : "f"(r1), "f"(r0));
           asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l23) : "f"(r3), "f"(r2));
-          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(hbase + off), "r"(h01), "r"(h23) : "memory");
-          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(hbase + K::CONV_HALF + off), "r"(l01), "r"(l23)
-                       : "memory");
+          *reinterpret_cast<uint2*>(hbase + i * istep) = make_uint2(h01, h23);
+          *reinterpret_cast<uint2*>(hbase + K::CONV_HALF + i * istep) = make_uint2(l01, l23);
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&raw_empty[rs]);
