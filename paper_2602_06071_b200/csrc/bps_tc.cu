@@ -45,22 +45,19 @@ struct Cfg {
   static constexpr int BN = BN_;  // data columns per CTA; TMEM = D (NMT·BN) + S (NMT·BN)
   static constexpr int ESZ = F32 ? 4 : 2;
   static constexpr int RAW_STAGE = kBK * BN * ESZ;
-  static constexpr int CONV_HALF = kBK * BN * 2;
-  static constexpr int CONV_STAGE = F32 ? 2 * CONV_HALF : 0;
-  static constexpr int NCONV = F32 ? 3 : 0;
+  static constexpr int CONV_HALF = kBK * BN * 2;  // fp32: hi and lo bf16 tiles overwrite the raw stage in place
   static constexpr int BAND_STAGE = NMT * kBandTile;
   static constexpr int NBAND = (NMT == 1 && !F32) ? 3 : 2;
   static constexpr int BUDGET = 210 * 1024;
-  static constexpr int NRAW_FIT = (BUDGET - NCONV * CONV_STAGE - NBAND * BAND_STAGE) / RAW_STAGE;
+  static constexpr int NRAW_FIT = (BUDGET - NBAND * BAND_STAGE) / RAW_STAGE;
   static constexpr int NRAW = NRAW_FIT > 8 ? 8 : NRAW_FIT;
   static constexpr int OFF_RAW = 0;
-  static constexpr int OFF_CONV = OFF_RAW + NRAW * RAW_STAGE;
-  static constexpr int OFF_BAND = OFF_CONV + NCONV * CONV_STAGE;
+  static constexpr int OFF_BAND = OFF_RAW + NRAW * RAW_STAGE;
   static constexpr int OFF_CKEY = OFF_BAND + NBAND * BAND_STAGE;  // [2][256] u64 per-block combo keys
   static constexpr int OFF_CROW = OFF_CKEY + 2 * 256 * 8;          // [2][256] u32 per-block band-row bases
   static constexpr int OFF_BAR = OFF_CROW + 2 * 256 * 4;
-  // raw full/empty, conv full/empty, band full/empty, acc full, acc free
-  static constexpr int NBARS = 2 * NRAW + 2 * NCONV + 2 * NBAND + 2;
+  // raw full/empty, conv full (fp32: per raw stage), band full/empty, acc full, acc free
+  static constexpr int NBARS = 3 * NRAW + 2 * NBAND + 2;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBARS * 8;
   static constexpr int SMEM = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
   static constexpr int NWARPS = F32 ? 24 : 16;
@@ -103,9 +100,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = raw_full + K::NRAW;
-  uint64_t* conv_full = raw_empty + K::NRAW;
-  uint64_t* conv_empty = conv_full + K::NCONV;
-  uint64_t* band_full = conv_empty + K::NCONV;
+  uint64_t* conv_full = raw_empty + K::NRAW;  // fp32: stage converted in place, ready for the MMA
+  uint64_t* band_full = conv_full + K::NRAW;
   uint64_t* band_empty = band_full + K::NBAND;
   uint64_t* acc_full = band_empty + K::NBAND;
   uint64_t* acc_free = acc_full + 1;
@@ -129,11 +125,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < K::NRAW; ++i) {
       ptx::mbar_init(&raw_full[i], 1);
-      ptx::mbar_init(&raw_empty[i], F32 ? K::NCONVT : 1);
-    }
-    for (int i = 0; i < K::NCONV; ++i) {
+      ptx::mbar_init(&raw_empty[i], 1);
       ptx::mbar_init(&conv_full[i], K::NCONVT);
-      ptx::mbar_init(&conv_empty[i], 1);
     }
     for (int i = 0; i < K::NBAND; ++i) {
       ptx::mbar_init(&band_full[i], K::NBANDT);
@@ -188,10 +181,10 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         int ds = 0, bs = 0;
         uint32_t dph = 0, bph = 0, fph = 0;
         uint64_t* dfull = F32 ? conv_full : raw_full;
-        uint64_t* dempty = F32 ? conv_empty : raw_empty;
-        constexpr int NDS = F32 ? K::NCONV : K::NRAW;
-        const uint32_t data_base = ptx::smem_u32(smem + (F32 ? K::OFF_CONV : K::OFF_RAW));
-        constexpr int DSTAGE = F32 ? K::CONV_STAGE : K::RAW_STAGE;
+        uint64_t* dempty = raw_empty;
+        constexpr int NDS = K::NRAW;
+        const uint32_t data_base = ptx::smem_u32(smem + K::OFF_RAW);
+        constexpr int DSTAGE = K::RAW_STAGE;
         const uint32_t band_base = ptx::smem_u32(smem + K::OFF_BAND);
         bool first_group = true;
         for (int64_t q = P; q < P + L; ++q) {
@@ -428,17 +421,18 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         istep = (uint32_t)(RPI / 8) * 1024u;
       }
       (void)off_odd;
-      int rs = 0, cs = 0;
-      uint32_t rph = 0, cph = 0;
+      int rs = 0;
+      uint32_t rph = 0;
       const int64_t total = L * nk;
       for (int64_t it = 0; it < total; ++it) {
         ptx::mbar_wait(&raw_full[rs], rph);
-        ptx::mbar_wait(&conv_empty[cs], cph ^ 1);
-        const float4* rawp = reinterpret_cast<const float4*>(smem + K::OFF_RAW + rs * K::RAW_STAGE) + cv;
-        uint8_t* hbase = smem + K::OFF_CONV + cs * K::CONV_STAGE + off_even;
+        uint8_t* stage = smem + K::OFF_RAW + rs * K::RAW_STAGE;
+        const float4* rawp = reinterpret_cast<const float4*>(stage) + cv;
         float4 a[NIT];
 #pragma unroll
         for (int i = 0; i < NIT; ++i) a[i] = rawp[i * NT];
+        ptx::named_bar_sync(2, NT);  // every converter has read its part: the stage can be overwritten
+        uint8_t* hbase = stage + off_even;
 #pragma unroll
         for (int i = 0; i < NIT; ++i) {
           uint32_t h01, h23, l01, l23;
@@ -452,10 +446,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
           *reinterpret_cast<uint2*>(hbase + K::CONV_HALF + i * istep) = make_uint2(l01, l23);
         }
         ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&raw_empty[rs]);
-        ptx::mbar_arrive(&conv_full[cs]);
+        ptx::mbar_arrive(&conv_full[rs]);
         if (++rs == K::NRAW) rs = 0, rph ^= 1;
-        if (++cs == K::NCONV) cs = 0, cph ^= 1;
       }
     }
   }
