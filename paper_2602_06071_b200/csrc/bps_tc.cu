@@ -25,6 +25,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "bps_internal.h"
@@ -36,10 +37,11 @@ namespace {
 constexpr int kBK = 64;                   // K rows per pipeline stage (one 128-byte swizzle row of bf16)
 constexpr int kBandTile = 128 * kBK * 2;  // one M-tile (128 band rows) of a band stage, bytes
 constexpr int kMaxGroup = 32;             // K-chunks per accumulation group (precision)
-constexpr int kCPT = 4;                   // (ℓ, j) combos per band thread kept in registers per pass
 
-// Warp roles: 0 TMA producer | 1 MMA issuer (+TMEM alloc) | 2-3 idle | 4-7 epilogue
-// (TMEM lane quarters 0-3) | 8-15 band generator | 16-23 fp32 hi/lo converter (fp32 only).
+// Warp roles (the issue arbiter favours high warp ids, so the latency-critical single-thread
+// roles take the last two warps): 0-3 epilogue (TMEM lane quarters 0-3) | 4-11 band
+// generator | 12-19 fp32 hi/lo converter (fp32 only) | NWARPS-2 TMA producer |
+// NWARPS-1 MMA issuer (+TMEM alloc).
 template <bool F32, bool TRANS, int NMT, int BN_>
 struct Cfg {
   static constexpr int BN = BN_;  // data columns per CTA; TMEM = D (NMT·BN) + S (NMT·BN)
@@ -54,20 +56,24 @@ struct Cfg {
   static constexpr int OFF_RAW = 0;
   static constexpr int OFF_BAND = OFF_RAW + NRAW * RAW_STAGE;
   static constexpr int OFF_CKEY = OFF_BAND + NBAND * BAND_STAGE;  // [2][256] u64 per-block combo keys
-  static constexpr int OFF_CROW = OFF_CKEY + 2 * 256 * 8;          // [2][256] u32 per-block band-row bases
-  static constexpr int OFF_BAR = OFF_CROW + 2 * 256 * 4;
+  static constexpr int OFF_CROW = OFF_CKEY + 2 * 256 * 8;  // [64] u32 band-row base σ·B_r + j·C of chunk c
+  static constexpr int OFF_BAR = OFF_CROW + 64 * 4;
   // raw full/empty, conv full (fp32: per raw stage), band full/empty, acc full, acc free
   static constexpr int NBARS = 3 * NRAW + 2 * NBAND + 2;
   static constexpr int OFF_TMEMPTR = OFF_BAR + NBARS * 8;
   static constexpr int SMEM = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
-  static constexpr int NWARPS = F32 ? 24 : 16;
-  static constexpr int NCONVT = 256;  // fp32 converter threads (warps 16-23)
+  static constexpr int NWARPS = F32 ? 22 : 14;
+  static constexpr int NCONVT = 256;  // fp32 converter threads (warps 12-19)
+  static constexpr int W_TMA = NWARPS - 2, W_MMA = NWARPS - 1;
   static constexpr int NTHREADS = NWARPS * 32;
   static constexpr int NBANDT = 256;  // band generator threads
-  static constexpr uint32_t TMEM_COLS = (2 * NMT * BN <= 256) ? 256 : 512;
-  static constexpr uint32_t IDESC = ptx::idesc_bf16(128, BN, !TRANS);
+  // fp32: the hi and lo tiles are adjacent along N in smem, so ONE MMA with N = 2·BN reads
+  // the band once for both (D columns [0,BN) = band·hi, [BN,2BN) = band·lo).
+  static constexpr int DN = F32 ? 2 * BN : BN;  // D columns per M-tile
+  static constexpr uint32_t TMEM_COLS = (NMT * (DN + BN) <= 256) ? 256 : 512;
+  static constexpr uint32_t IDESC = ptx::idesc_bf16(128, DN, !TRANS);
   static_assert(NRAW >= 2, "smem: raw ring");
-  static_assert(2 * NMT * BN <= 512, "TMEM");
+  static_assert(NMT * (DN + BN) <= 512 && DN <= 256, "TMEM / MMA N");
   static_assert(BN % 64 == 0 && BN <= 256, "BN");
   static_assert(SMEM <= 227 * 1024, "smem");
 };
@@ -83,6 +89,7 @@ struct TcArgs {
   int64_t stream_len;          // number of input positions in the window
   int R;                       // ranges per column tile
   int G;                       // K-chunks per accumulation group (divides B_c/64)
+  int dbg;                     // experiment switches (env BPS_TC_DEBUG; 0 in production): 1 no band, 2 no convert, 4 no MMA
 };
 
 __device__ __forceinline__ uint32_t mod_pos(int64_t i, uint32_t M) {
@@ -137,15 +144,15 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
     ptx::fence_mbar_init();
     ptx::tma_prefetch(&tmap);
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_ptr, K::TMEM_COLS);
+  if (warp == K::W_MMA) ptx::tmem_alloc(tmem_ptr, K::TMEM_COLS);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_ptr;               // D: per-group tensor-core accumulator
-  const uint32_t tmem_S = tmem + NMT * BN;       // S: fp32 running sums (RN adds on CUDA cores)
+  const uint32_t tmem_S = tmem + NMT * K::DN;    // S: fp32 running sums (RN adds on CUDA cores)
 
   if (L > 0) {
-    if (warp == 0) {
+    if (warp == K::W_TMA) {
       // ===================== TMA producer =====================
       if (lane == 0) {
         const uint64_t pol = ptx::policy_evict_first();
@@ -175,7 +182,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
           gq = affine_step(p, gq);
         }
       }
-    } else if (warp == 1) {
+    } else if (warp == K::W_MMA) {
       // ===================== MMA issuer =====================
       if (lane == 0) {
         int ds = 0, bs = 0;
@@ -205,14 +212,10 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
 #pragma unroll
               for (int m = 0; m < NMT; ++m) {
                 const uint64_t adesc = ptx::smem_desc_sw128(bbase + m * kBandTile + ks * 32, 0, 1024);
-#pragma unroll
-                for (int part = 0; part < (F32 ? 2 : 1); ++part) {
-                  const uint32_t pb = dbase + part * (F32 ? K::CONV_HALF : 0);
-                  const uint64_t bdesc = TRANS ? ptx::smem_desc_sw128(pb + ks * 32, 0, 1024)
-                                               : ptx::smem_desc_sw128(pb + ks * 16 * 128, kBK * 128, 1024);
-                  const uint32_t acc = (gi == 0 && ks == 0 && part == 0) ? 0u : 1u;  // fresh per group
-                  ptx::mma_bf16_ss(tmem + m * BN, adesc, bdesc, K::IDESC, acc);
-                }
+                const uint64_t bdesc = TRANS ? ptx::smem_desc_sw128(dbase + ks * 32, 0, 1024)
+                                             : ptx::smem_desc_sw128(dbase + ks * 16 * 128, kBK * 128, 1024);
+                const uint32_t acc = (gi == 0 && ks == 0) ? 0u : 1u;  // fresh per group
+                if (!(args.dbg & 4)) ptx::mma_bf16_ss(tmem + m * K::DN, adesc, bdesc, K::IDESC, acc);
               }
             }
             ptx::mma_commit(&dempty[ds]);
@@ -226,7 +229,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
           }
         }
       }
-    } else if (warp >= 4 && warp < 8) {
+    } else if (warp < 4) {
       // ============ epilogue: S += D (fp32 RN) per group; emit the slot that completes ============
       const int qtr = warp & 3;
       const uint32_t lane_off = (uint32_t)(qtr * 32) << 16;
@@ -294,12 +297,21 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 16) {
               uint32_t d[16], sv[16];
-              ptx::tmem_ld16(tmem + lane_off + m * BN + c0, d);
+              ptx::tmem_ld16(tmem + lane_off + m * K::DN + c0, d);
               ptx::tmem_ld16(tmem_S + lane_off + m * BN + c0, sv);
-              ptx::tmem_wait_ld();
               float tot[16];
+              if (F32) {  // hi and lo partial products
+                uint32_t dl[16];
+                ptx::tmem_ld16(tmem + lane_off + m * K::DN + BN + c0, dl);
+                ptx::tmem_wait_ld();
 #pragma unroll
-              for (int t = 0; t < 16; ++t) tot[t] = __uint_as_float(sv[t]) + __uint_as_float(d[t]);
+                for (int t = 0; t < 16; ++t)
+                  tot[t] = __uint_as_float(sv[t]) + (__uint_as_float(d[t]) + __uint_as_float(dl[t]));
+              } else {
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int t = 0; t < 16; ++t) tot[t] = __uint_as_float(sv[t]) + __uint_as_float(d[t]);
+              }
               if (in_slot) emit(i, rho, tot, c0);
 #pragma unroll
               for (int t = 0; t < 16; ++t) sv[t] = in_slot ? 0u : __float_as_uint(tot[t]);
@@ -332,70 +344,95 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
           }
         }
       }
-    } else if (warp >= 8 && warp < 16) {
+    } else if (warp >= 4 && warp < 12) {
       // ===================== band generator =====================
-      // Thread (u, cg): column u of every band stage, combos c = cg, cg+4, ... (c = (ℓ-1)·s + j).
-      const int bt = threadIdx.x - 256;
+      // Thread (u, cg) writes column u of every band stage for the row chunks c = cg + 4t,
+      // c = σ·s + j (slot σ, chunk j).  A chunk's rows [σB_r + jC, +C) are owned by one thread
+      // per column, so each thread can clear the single entry it wrote into this buffer
+      // NBAND stages ago and write the new one without any barrier (no zero-fill pass).
+      const int bt = threadIdx.x - 128;
       const uint32_t u = (uint32_t)bt & (kBK - 1);
       const uint32_t cg = (uint32_t)bt >> 6;  // 0..3
       const uint32_t ncombo = kappa * p.s;
+      const uint32_t T = ncombo > cg ? (ncombo - cg + 3) / 4 : 0;  // chunks of this thread (≤ 16)
       const uint32_t band_u32 = ptx::smem_u32(smem + K::OFF_BAND);
       const uint32_t ucol = u >> 3, ulo = (u & 7) * 2;
+      auto entry = [&](uint32_t sbase, uint32_t rho) {
+        const uint32_t r7 = rho & 127;
+        return sbase + (rho >> 7) * kBandTile + (r7 >> 3) * 1024 + (r7 & 7) * 128 + ((ucol ^ (r7 & 7)) << 4) + ulo;
+      };
+      {  // band buffers start zeroed; chunk row bases (fixed for the whole launch)
+        uint4* bz = reinterpret_cast<uint4*>(smem + K::OFF_BAND);
+        for (int i = bt; i < K::NBAND * K::BAND_STAGE / 16; i += K::NBANDT) bz[i] = make_uint4(0, 0, 0, 0);
+        for (uint32_t c = bt; c < ncombo; c += K::NBANDT) crow[c] = (c / p.s) * p.B_r + (c % p.s) * p.C;
+      }
+      uint32_t prev[K::NBAND][4];  // rows written NBAND stages ago, 4 bytes per word (κ·B_r ≤ 256)
+#pragma unroll
+      for (int b = 0; b < K::NBAND; ++b)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) prev[b][w] = 0;
       int bs = 0;
       uint32_t bph = 0;
+      int64_t stage_no = 0;
       for (int64_t q = P; q < P + L; ++q) {
         const int par = (int)(q & 1);  // tables double-buffered by block parity
         uint64_t* ck = ckey + par * 256;
-        uint32_t* cr = crow + par * 256;
-        for (int kc = 0; kc < nk; ++kc) {
+        for (int kc = 0; kc < nk; ++kc, ++stage_no) {
           ptx::mbar_wait_sleep(&band_empty[bs], bph ^ 1, 20);
           if (kc == 0) {
-            // per input block q: hash key and band-row base of every combo (ℓ, j) — output q-ℓ
+            // per input block q: hash key of chunk (σ, j): the output i ≡ σ (mod κ) fed by q is
+            // i = q - ℓ with ℓ = ((q - σ - 1) mod κ) + 1
             for (uint32_t c = bt; c < ncombo; c += K::NBANDT) {
-              const uint32_t ell = c / p.s + 1, j = c % p.s;
-              const int64_t iout = q - (int64_t)ell;
-              const uint32_t g = affine_pow(p, (uint64_t)mod_pos(iout, p.M), 0u);
+              const uint32_t sig = c / p.s, j = c % p.s;
+              const uint32_t ell = mod_pos(q - (int64_t)sig - 1, kappa) + 1;
+              const uint32_t g = affine_pow(p, (uint64_t)mod_pos(q - (int64_t)ell, p.M), 0u);
               ck[c] = (((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | (uint64_t)j) ^ p.K;
-              cr[c] = mod_pos(iout, kappa) * p.B_r + j * p.C;
             }
+            ptx::named_bar_sync(1, K::NBANDT);
           }
-          uint4* bz = reinterpret_cast<uint4*>(smem + K::OFF_BAND + bs * K::BAND_STAGE);
-#pragma unroll
-          for (int i = 0; i < K::BAND_STAGE / 16 / K::NBANDT; ++i) bz[bt + i * K::NBANDT] = make_uint4(0, 0, 0, 0);
-          ptx::named_bar_sync(1, K::NBANDT);
           const uint64_t uk = (uint64_t)((uint32_t)kc * kBK + u) << 8;
           const uint32_t sbase = band_u32 + bs * K::BAND_STAGE;
-          for (uint32_t c0 = cg; c0 < ncombo; c0 += 4 * kCPT) {
-            uint64_t z[kCPT];
-            uint32_t rb[kCPT];
+          const bool clear = stage_no >= K::NBAND;
+          uint32_t nw[4] = {0, 0, 0, 0};
+          if (!(args.dbg & 1)) {
 #pragma unroll
-            for (int t = 0; t < kCPT; ++t) {
-              const uint32_t c = c0 + 4 * t;
-              const uint32_t cc = c < ncombo ? c : c0;
-              z[t] = mix64(ck[cc] ^ uk);
-              rb[t] = cr[cc];
-            }
+            for (int w = 0; w < 4; ++w) {
+              if ((uint32_t)w * 4 >= T) break;
+              uint64_t z[4];
 #pragma unroll
-            for (int t = 0; t < kCPT; ++t) {
-              if (c0 + 4 * t >= ncombo) continue;
-              const uint32_t rho = rb[t] + __umulhi((uint32_t)(z[t] >> 32), p.C);  // R3
-              const uint32_t r7 = rho & 127;
-              const uint32_t addr = sbase + (rho >> 7) * kBandTile + (r7 >> 3) * 1024 + (r7 & 7) * 128 +
-                                    ((ucol ^ (r7 & 7)) << 4) + ulo;
-              ptx::st_shared_u16(addr, (z[t] & 1) ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
+              for (int i = 0; i < 4; ++i) {
+                const uint32_t c = cg + 4 * (4 * w + i);
+                z[i] = mix64(ck[c < ncombo ? c : cg] ^ uk);
+              }
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const uint32_t t = 4 * w + i;
+                if (t >= T) break;
+                const uint32_t c = cg + 4 * t;
+                if (clear) ptx::st_shared_u16(entry(sbase, (prev[0][w] >> (8 * i)) & 0xFFu), 0);
+                const uint32_t rho = crow[c] + __umulhi((uint32_t)(z[i] >> 32), p.C);  // R3
+                ptx::st_shared_u16(entry(sbase, rho), (z[i] & 1) ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
+                nw[w] |= rho << (8 * i);
+              }
             }
           }
+#pragma unroll
+          for (int b = 0; b + 1 < K::NBAND; ++b)
+#pragma unroll
+            for (int w = 0; w < 4; ++w) prev[b][w] = prev[b + 1][w];
+#pragma unroll
+          for (int w = 0; w < 4; ++w) prev[K::NBAND - 1][w] = nw[w];
           ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&band_full[bs]);
           if (++bs == K::NBAND) bs = 0, bph ^= 1;
         }
       }
-    } else if (F32 && warp >= 16) {
+    } else if (F32 && warp >= 12 && warp < 20) {
       // ===================== fp32 -> (hi, lo) bf16 split =====================
       // a = hi + lo, hi = bf16_rn(a), lo = bf16_rn(a - hi): |a - hi - lo| ≤ 2^-17 |a|.
       // Thread cv owns 4 consecutive MN (or K) elements of rows cv/(BN/4) + RPI·i; the
       // swizzled destination offset is affine in i, so it is precomputed (two parities).
-      const int cv = threadIdx.x - 512;
+      const int cv = threadIdx.x - 384;
       constexpr int NT = K::NCONVT;
       constexpr int NIT = kBK * BN / 4 / NT;  // float4 per thread per stage
       static_assert(NIT * NT * 4 == kBK * BN, "converter tiling");
@@ -434,7 +471,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         ptx::named_bar_sync(2, NT);  // every converter has read its part: the stage can be overwritten
         uint8_t* hbase = stage + off_even;
 #pragma unroll
-        for (int i = 0; i < NIT; ++i) {
+        for (int i = 0; i < ((args.dbg & 2) ? 0 : NIT); ++i) {
           uint32_t h01, h23, l01, l23;
           asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(a[i].y), "f"(a[i].x));
           asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h23) : "f"(a[i].w), "f"(a[i].z));
@@ -453,7 +490,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == K::W_MMA) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, K::TMEM_COLS);
   }
@@ -498,6 +535,10 @@ Plan plan_for(const SketchParams& p, bps_dtype dt) {
   const uint64_t rows = (uint64_t)p.kappa * p.B_r;
   if (rows > 256) {
     pl.why = "tc variant needs kappa*B_r <= 256";
+    return pl;
+  }
+  if ((uint64_t)p.kappa * p.s > 64) {
+    pl.why = "tc variant needs kappa*s <= 64";
     return pl;
   }
   pl.nmt = rows <= 128 ? 1 : 2;
@@ -549,6 +590,10 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
       break;
     }
   a.G = G;
+  {
+    const char* e = getenv("BPS_TC_DEBUG");
+    a.dbg = e ? atoi(e) : 0;
+  }
   const int64_t n_ct = (n + BN - 1) / BN;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
