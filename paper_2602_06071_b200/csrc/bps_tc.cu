@@ -25,8 +25,11 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "bps_internal.h"
 #include "bps_ptx.cuh"
@@ -36,7 +39,7 @@ namespace {
 
 constexpr int kBK = 64;                   // K rows per pipeline stage (one 128-byte swizzle row of bf16)
 constexpr int kBandTile = 128 * kBK * 2;  // one M-tile (128 band rows) of a band stage, bytes
-constexpr int kMaxGroup = 32;             // K-chunks per accumulation group (precision)
+constexpr int kMaxGroup = 128;            // K-chunks per accumulation group (precision)
 
 // Warp roles (the issue arbiter favours high warp ids, so the latency-critical single-thread
 // roles take the last two warps): 0-3 epilogue (TMEM lane quarters 0-3) | 4-11 band
@@ -89,7 +92,18 @@ struct TcArgs {
   int64_t stream_len;          // number of input positions in the window
   int R;                       // ranges per column tile
   int G;                       // K-chunks per accumulation group (divides B_c/64)
-  int dbg;                     // experiment switches (env BPS_TC_DEBUG; 0 in production): 1 no band, 2 no convert, 4 no MMA
+  int dbg;  // experiment switches (env BPS_TC_DEBUG; 0 in production): 1 no band, 2 no convert, 4 no MMA,
+            // 8 cycle trace, 16 no band proxy fence, 32 band without hashing
+  unsigned long long* trace;   // dbg & 8: per-CTA cycle counters (16 per CTA), else nullptr
+};
+
+// cycle accounting for the BPS_TC_DEBUG=8 trace (compiled in, inactive unless trace != nullptr)
+struct Tr {
+  unsigned long long* t;
+  __device__ __forceinline__ unsigned long long now() const { return t ? clock64() : 0ull; }
+  __device__ __forceinline__ void add(int slot, unsigned long long t0) const {
+    if (t) t[slot] += clock64() - t0;
+  }
 };
 
 __device__ __forceinline__ uint32_t mod_pos(int64_t i, uint32_t M) {
@@ -155,6 +169,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
     if (warp == K::W_TMA) {
       // ===================== TMA producer =====================
       if (lane == 0) {
+        const Tr tr{args.trace ? args.trace + blockIdx.x * 16 : nullptr};
+        const unsigned long long tstart = tr.now();
         const uint64_t pol = ptx::policy_evict_first();
         uint32_t gq = affine_pow(p, (uint64_t)mod_pos(P, p.M), 0u);
         int s = 0;
@@ -162,7 +178,9 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         for (int64_t q = P; q < P + L; ++q) {
           const int64_t row0 = args.range_mode ? (q - (args.pos_begin + 1)) * (int64_t)p.B_c : (int64_t)gq * p.B_c;
           for (int kc = 0; kc < nk; ++kc) {
+            const unsigned long long t0 = tr.now();
             ptx::mbar_wait_sleep(&raw_empty[s], ph ^ 1, 20);
+            tr.add(0, t0);
             ptx::mbar_arrive_expect_tx(&raw_full[s], K::RAW_STAGE);
             uint8_t* dst = smem + K::OFF_RAW + s * K::RAW_STAGE;
             const int32_t r = (int32_t)(row0 + kc * kBK);
@@ -181,10 +199,13 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
           }
           gq = affine_step(p, gq);
         }
+        tr.add(1, tstart);
       }
     } else if (warp == K::W_MMA) {
       // ===================== MMA issuer =====================
       if (lane == 0) {
+        const Tr tr{args.trace ? args.trace + blockIdx.x * 16 : nullptr};
+        const unsigned long long tstart = tr.now();
         int ds = 0, bs = 0;
         uint32_t dph = 0, bph = 0, fph = 0;
         uint64_t* dfull = F32 ? conv_full : raw_full;
@@ -198,12 +219,18 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
           for (int kc = 0; kc < nk; ++kc) {
             const int gi = kc % G;
             if (gi == 0 && !first_group) {  // D must have been folded into S
+              const unsigned long long t0 = tr.now();
               ptx::mbar_wait(acc_free, fph);
+              tr.add(2, t0);
               fph ^= 1;
               ptx::tc_fence_after();
             }
+            unsigned long long t0 = tr.now();
             ptx::mbar_wait(&dfull[ds], dph);
+            tr.add(3, t0);
+            t0 = tr.now();
             ptx::mbar_wait(&band_full[bs], bph);
+            tr.add(4, t0);
             ptx::tc_fence_after();
             const uint32_t dbase = data_base + ds * DSTAGE;
             const uint32_t bbase = band_base + bs * K::BAND_STAGE;
@@ -228,6 +255,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
             }
           }
         }
+        tr.add(5, tstart);
       }
     } else if (warp < 4) {
       // ============ epilogue: S += D (fp32 RN) per group; emit the slot that completes ============
@@ -282,11 +310,15 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
       };
       uint32_t aph = 0;
       const int ngrp = nk / G;
+      const Tr tr{(args.trace && threadIdx.x == 0) ? args.trace + blockIdx.x * 16 : nullptr};
+      const unsigned long long tstart = tr.now();
       for (int64_t q = P; q < P + L; ++q) {
         const int64_t i = q - (int64_t)kappa;  // output completed by input block q
         const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
         for (int gix = 0; gix < ngrp; ++gix) {
+          const unsigned long long t0 = tr.now();
           ptx::mbar_wait_sleep(acc_full, aph, 32);
+          tr.add(9, t0);
           aph ^= 1;
           ptx::tc_fence_after();
           const bool last = gix == ngrp - 1;
@@ -323,6 +355,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
           ptx::mbar_arrive(acc_free);
         }
       }
+      tr.add(10, tstart);
       // range end: outputs P+L-κ .. P+L-2 hold partial sums in S
       for (int64_t i = P + L - (int64_t)kappa; i <= P + L - 2; ++i) {
         const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
@@ -374,11 +407,16 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
       int bs = 0;
       uint32_t bph = 0;
       int64_t stage_no = 0;
+      const Tr tr{(args.trace && bt == 0) ? args.trace + blockIdx.x * 16 : nullptr};
+      const unsigned long long tstart = tr.now();
       for (int64_t q = P; q < P + L; ++q) {
         const int par = (int)(q & 1);  // tables double-buffered by block parity
         uint64_t* ck = ckey + par * 256;
         for (int kc = 0; kc < nk; ++kc, ++stage_no) {
+          unsigned long long t0 = tr.now();
           ptx::mbar_wait_sleep(&band_empty[bs], bph ^ 1, 20);
+          tr.add(6, t0);
+          t0 = tr.now();
           if (kc == 0) {
             // per input block q: hash key of chunk (σ, j): the output i ≡ σ (mod κ) fed by q is
             // i = q - ℓ with ℓ = ((q - σ - 1) mod κ) + 1
@@ -389,6 +427,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
               ck[c] = (((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | (uint64_t)j) ^ p.K;
             }
             ptx::named_bar_sync(1, K::NBANDT);
+            tr.add(7, t0);
           }
           const uint64_t uk = (uint64_t)((uint32_t)kc * kBK + u) << 8;
           const uint32_t sbase = band_u32 + bs * K::BAND_STAGE;
@@ -402,7 +441,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 const uint32_t c = cg + 4 * (4 * w + i);
-                z[i] = mix64(ck[c < ncombo ? c : cg] ^ uk);
+                z[i] = (args.dbg & 32) ? (ck[c < ncombo ? c : cg] ^ uk) : mix64(ck[c < ncombo ? c : cg] ^ uk);
               }
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
@@ -422,11 +461,12 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
             for (int w = 0; w < 4; ++w) prev[b][w] = prev[b + 1][w];
 #pragma unroll
           for (int w = 0; w < 4; ++w) prev[K::NBAND - 1][w] = nw[w];
-          ptx::fence_proxy_async_smem();
+          if (!(args.dbg & 16)) ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&band_full[bs]);
           if (++bs == K::NBAND) bs = 0, bph ^= 1;
         }
       }
+      tr.add(8, tstart);
     } else if (F32 && warp >= 12 && warp < 20) {
       // ===================== fp32 -> (hi, lo) bf16 split =====================
       // a = hi + lo, hi = bf16_rn(a), lo = bf16_rn(a - hi): |a - hi - lo| ≤ 2^-17 |a|.
@@ -461,8 +501,12 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
       int rs = 0;
       uint32_t rph = 0;
       const int64_t total = L * nk;
+      const Tr tr{(args.trace && cv == 0) ? args.trace + blockIdx.x * 16 : nullptr};
+      const unsigned long long tstart = tr.now();
       for (int64_t it = 0; it < total; ++it) {
+        const unsigned long long t0 = tr.now();
         ptx::mbar_wait(&raw_full[rs], rph);
+        tr.add(11, t0);
         uint8_t* stage = smem + K::OFF_RAW + rs * K::RAW_STAGE;
         const float4* rawp = reinterpret_cast<const float4*>(stage) + cv;
         float4 a[NIT];
@@ -486,6 +530,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         ptx::mbar_arrive(&conv_full[rs]);
         if (++rs == K::NRAW) rs = 0, rph ^= 1;
       }
+      tr.add(12, tstart);
     }
   }
   ptx::tc_fence_before();
@@ -594,6 +639,7 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     const char* e = getenv("BPS_TC_DEBUG");
     a.dbg = e ? atoi(e) : 0;
   }
+  a.trace = nullptr;
   const int64_t n_ct = (n + BN - 1) / BN;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -636,8 +682,29 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
   auto kern = bps_tc_kernel<F32, TRANS, NMT, BN_>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
   if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  if (a.dbg & 8) {  // debug trace: per-CTA cycle counters, printed to stderr (synchronises)
+    cudaMalloc(&a.trace, (size_t)grid * 16 * 8);
+    cudaMemsetAsync(a.trace, 0, (size_t)grid * 16 * 8, st);
+  }
   kern<<<(unsigned)grid, K::NTHREADS, K::SMEM, st>>>(tm, a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (a.trace) {
+    std::vector<unsigned long long> h((size_t)grid * 16);
+    cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const char* names[13] = {"tma_wait_empty", "tma_total", "mma_wait_accfree", "mma_wait_data", "mma_wait_band",
+                             "mma_total", "band_wait_empty", "band_table", "band_total", "epi_wait_accfull",
+                             "epi_total", "conv_wait_raw", "conv_total"};
+    for (int k = 0; k < 13; ++k) {
+      double sum = 0, mx = 0;
+      for (int64_t c = 0; c < grid; ++c) {
+        sum += (double)h[c * 16 + k];
+        mx = std::max(mx, (double)h[c * 16 + k]);
+      }
+      fprintf(stderr, "[bps trace] %-18s mean %12.0f  max %12.0f cycles\n", names[k], sum / grid, mx);
+    }
+    cudaFree(a.trace);
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("bps_tc_kernel launch: ") + cudaGetErrorString(e));
   return BPS_OK;

@@ -1,6 +1,6 @@
 #!/bin/bash
 # timing experiments with parts of the tc kernel disabled (results are wrong by design)
 for c in ${CONFIGS:-ls grad}; do
-for f in 0 1 2 3 4 5 7; do
+for f in ${FLAGS:-0 1 2 3 4 5 7}; do
   BPS_TC_DEBUG=$f timeout 300 python bench.py --config $c --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c dbg=$f', round(d['value'],1), 'GB/s', round(d['ms_per_step'],3), 'ms')"
 done; done
