@@ -39,6 +39,9 @@ def parse():
     ap.add_argument("--config", default="ls")
     ap.add_argument("--variant", default="auto", choices=["auto", "sparse", "tc"])
     ap.add_argument("--kind", default="gaussian", choices=["gaussian", "coherent", "lowrank"])
+    ap.add_argument("--shard", default="column", choices=["column", "block"],
+                    help="column: weak scaling, every rank its own n-column batch (no collective); "
+                         "block: strong scaling of one d×n problem sharded along the wiring orbit + all-gather")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -188,12 +191,24 @@ def main():
     n = cfg.n
     tdt = torch.float32 if cfg.dtype == "f32" else torch.bfloat16
     sk = Sketch(**cfg.sketch_args())
-    A = synth.device_matrix(args.kind, cfg.d, n, seed=1000 + rank, M=cfg.M, dtype=tdt, device=dev)
-    Y = torch.empty((cfg.k, n), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    if args.shard == "block" and world > 1:
+        from paper_2602_06071_b200 import dist as D
 
-    def step():
-        sk.apply(A, out=Y, variant=args.variant)
+        p0, p1 = D.orbit_shard(cfg.M, world, rank)
+        nblk = (p1 - p0) + cfg.kappa - 1
+        # this rank's stacked input blocks (orbit positions p0+1 .. p1+κ-1), synthetic
+        A = synth.device_matrix(args.kind, nblk * cfg.B_c, n, seed=1000 + rank, M=nblk, dtype=tdt, device=dev)
+        Y = torch.empty((cfg.k, n), dtype=torch.float32, device=dev)
+
+        def step():
+            D.block_sharded_apply(sk, A, out=Y)
+    else:
+        A = synth.device_matrix(args.kind, cfg.d, n, seed=1000 + rank, M=cfg.M, dtype=tdt, device=dev)
+        Y = torch.empty((cfg.k, n), dtype=torch.float32, device=dev)
+
+        def step():
+            sk.apply(A, out=Y, variant=args.variant)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -223,14 +238,15 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_max = float(t.item())
     ms = total_max / args.steps
-    bytes_rank = cfg.roofline_bytes(n)
+    block = args.shard == "block" and world > 1
+    bytes_rank = cfg.roofline_bytes(n) if not block else cfg.roofline_bytes(n) // world
     value = world * bytes_rank / (ms / 1e3) / 1e9
     peak, peak_src = measured_peaks()
     achieved = bytes_rank / (statistics.mean(per) / 1e3) / 1e9
 
     # end-to-end through the public API with pinned host buffers (H2D + apply + D2H per step)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not block:
         max_e2e_bytes = 8 << 30
         n_e = n if bytes_rank <= max_e2e_bytes else max(128, int(n * max_e2e_bytes / bytes_rank) // 128 * 128)
         A_h = torch.empty((cfg.d, n_e), dtype=tdt, pin_memory=True)
@@ -276,14 +292,16 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if block else "weak",
             "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" else "bf16-in/f32-acc",
             "data": f"synthetic {args.kind} (torch Philox on device), seed {1000}+rank",
             "config": {"workload": cfg.name, "d": cfg.d, "k": cfg.k, "kappa": cfg.kappa, "s": cfg.s,
                        "n_per_gpu": n, "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c, "variant": args.variant,
-                       "parallelism": f"column-shard x{world} (no collective)",
+                       "parallelism": (f"orbit-block-shard x{world} + NCCL all_gather" if block
+                                       else f"column-shard x{world} (no collective)"),
                        "l2": "inputs larger than L2 (no flush needed)" if bytes_rank > (256 << 20) else "input fits L2"},
-            "columns_per_s": world * n / (ms / 1e3),
+            "columns_per_s": (n if block else world * n) / (ms / 1e3),
             "gbs_per_gpu": value / world,
             "frac_of_8tbs": value / world / 8000.0,
             "ms_min": min(per), "ms_median": statistics.median(per),

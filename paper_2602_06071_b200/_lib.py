@@ -6,7 +6,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libbps.so")
+# BPS_LIB may point at the instrumented build (libbps_instr.so) for experiments
+lib_path = os.environ.get("BPS_LIB") or os.path.join(_HERE, "libbps.so")
 
 BPS_OK = 0
 STATUS = {

@@ -13,6 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbps.so")
+LIB_INSTR = os.path.join(HERE, "libbps_instr.so")  # -DBPS_TC_INSTRUMENT: cycle trace + ablation switches
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -43,11 +44,13 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, instrument: bool = False) -> str:
+    out = LIB_INSTR if instrument else LIB
+    if not force and not instrument and not needs_build():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(HERE, "..", "include"), "-o", tmp, *sources()]
+    tmp = out + ".tmp"
+    extra = ["-DBPS_TC_INSTRUMENT"] if instrument else []
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(HERE, "..", "include"), "-o", tmp, *sources()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
@@ -57,9 +60,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, instrument="--instrument" in sys.argv))

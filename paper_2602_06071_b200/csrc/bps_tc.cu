@@ -98,13 +98,24 @@ struct TcArgs {
 };
 
 // cycle accounting for the BPS_TC_DEBUG=8 trace (compiled in, inactive unless trace != nullptr)
+#ifdef BPS_TC_INSTRUMENT
 struct Tr {
   unsigned long long* t;
+  __device__ __forceinline__ Tr(unsigned long long* p) : t(p) {}
   __device__ __forceinline__ unsigned long long now() const { return t ? clock64() : 0ull; }
   __device__ __forceinline__ void add(int slot, unsigned long long t0) const {
     if (t) t[slot] += clock64() - t0;
   }
 };
+#define BPS_DBG(x) (args.dbg & (x))
+#else
+struct Tr {  // production build: instrumentation compiled out
+  __device__ __forceinline__ Tr(unsigned long long*) {}
+  __device__ __forceinline__ unsigned long long now() const { return 0ull; }
+  __device__ __forceinline__ void add(int, unsigned long long) const {}
+};
+#define BPS_DBG(x) 0
+#endif
 
 __device__ __forceinline__ uint32_t mod_pos(int64_t i, uint32_t M) {
   int64_t r = i % (int64_t)M;
@@ -169,7 +180,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
     if (warp == K::W_TMA) {
       // ===================== TMA producer =====================
       if (lane == 0) {
-        const Tr tr{args.trace ? args.trace + blockIdx.x * 16 : nullptr};
+        const Tr tr(args.trace ? args.trace + blockIdx.x * 16 : nullptr);
         const unsigned long long tstart = tr.now();
         const uint64_t pol = ptx::policy_evict_first();
         uint32_t gq = affine_pow(p, (uint64_t)mod_pos(P, p.M), 0u);
@@ -204,7 +215,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
     } else if (warp == K::W_MMA) {
       // ===================== MMA issuer =====================
       if (lane == 0) {
-        const Tr tr{args.trace ? args.trace + blockIdx.x * 16 : nullptr};
+        const Tr tr(args.trace ? args.trace + blockIdx.x * 16 : nullptr);
         const unsigned long long tstart = tr.now();
         int ds = 0, bs = 0;
         uint32_t dph = 0, bph = 0, fph = 0;
@@ -242,7 +253,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
                 const uint64_t bdesc = TRANS ? ptx::smem_desc_sw128(dbase + ks * 32, 0, 1024)
                                              : ptx::smem_desc_sw128(dbase + ks * 16 * 128, kBK * 128, 1024);
                 const uint32_t acc = (gi == 0 && ks == 0) ? 0u : 1u;  // fresh per group
-                if (!(args.dbg & 4)) ptx::mma_bf16_ss(tmem + m * K::DN, adesc, bdesc, K::IDESC, acc);
+                if (!BPS_DBG(4)) ptx::mma_bf16_ss(tmem + m * K::DN, adesc, bdesc, K::IDESC, acc);
               }
             }
             ptx::mma_commit(&dempty[ds]);
@@ -310,7 +321,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
       };
       uint32_t aph = 0;
       const int ngrp = nk / G;
-      const Tr tr{(args.trace && threadIdx.x == 0) ? args.trace + blockIdx.x * 16 : nullptr};
+      const Tr tr((args.trace && threadIdx.x == 0) ? args.trace + blockIdx.x * 16 : nullptr);
       const unsigned long long tstart = tr.now();
       for (int64_t q = P; q < P + L; ++q) {
         const int64_t i = q - (int64_t)kappa;  // output completed by input block q
@@ -407,7 +418,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
       int bs = 0;
       uint32_t bph = 0;
       int64_t stage_no = 0;
-      const Tr tr{(args.trace && bt == 0) ? args.trace + blockIdx.x * 16 : nullptr};
+      const Tr tr((args.trace && bt == 0) ? args.trace + blockIdx.x * 16 : nullptr);
       const unsigned long long tstart = tr.now();
       for (int64_t q = P; q < P + L; ++q) {
         const int par = (int)(q & 1);  // tables double-buffered by block parity
@@ -433,7 +444,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
           const uint32_t sbase = band_u32 + bs * K::BAND_STAGE;
           const bool clear = stage_no >= K::NBAND;
           uint32_t nw[4] = {0, 0, 0, 0};
-          if (!(args.dbg & 1)) {
+          if (!BPS_DBG(1)) {
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
               if ((uint32_t)w * 4 >= T) break;
@@ -441,7 +452,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 const uint32_t c = cg + 4 * (4 * w + i);
-                z[i] = (args.dbg & 32) ? (ck[c < ncombo ? c : cg] ^ uk) : mix64(ck[c < ncombo ? c : cg] ^ uk);
+                z[i] = BPS_DBG(32) ? (ck[c < ncombo ? c : cg] ^ uk) : mix64(ck[c < ncombo ? c : cg] ^ uk);
               }
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
@@ -461,7 +472,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
             for (int w = 0; w < 4; ++w) prev[b][w] = prev[b + 1][w];
 #pragma unroll
           for (int w = 0; w < 4; ++w) prev[K::NBAND - 1][w] = nw[w];
-          if (!(args.dbg & 16)) ptx::fence_proxy_async_smem();
+          if (!BPS_DBG(16)) ptx::fence_proxy_async_smem();
           ptx::mbar_arrive(&band_full[bs]);
           if (++bs == K::NBAND) bs = 0, bph ^= 1;
         }
@@ -501,7 +512,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
       int rs = 0;
       uint32_t rph = 0;
       const int64_t total = L * nk;
-      const Tr tr{(args.trace && cv == 0) ? args.trace + blockIdx.x * 16 : nullptr};
+      const Tr tr((args.trace && cv == 0) ? args.trace + blockIdx.x * 16 : nullptr);
       const unsigned long long tstart = tr.now();
       for (int64_t it = 0; it < total; ++it) {
         const unsigned long long t0 = tr.now();
@@ -515,7 +526,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         ptx::named_bar_sync(2, NT);  // every converter has read its part: the stage can be overwritten
         uint8_t* hbase = stage + off_even;
 #pragma unroll
-        for (int i = 0; i < ((args.dbg & 2) ? 0 : NIT); ++i) {
+        for (int i = 0; i < (BPS_DBG(2) ? 0 : NIT); ++i) {
           uint32_t h01, h23, l01, l23;
           asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(a[i].y), "f"(a[i].x));
           asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h23) : "f"(a[i].w), "f"(a[i].z));
@@ -635,11 +646,18 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
       break;
     }
   a.G = G;
+  a.dbg = 0;
+  a.trace = nullptr;
+#ifdef BPS_TC_INSTRUMENT
   {
     const char* e = getenv("BPS_TC_DEBUG");
     a.dbg = e ? atoi(e) : 0;
   }
-  a.trace = nullptr;
+#endif
+  if (const char* e = getenv("BPS_TC_GROUP")) {  // tuning knob: K-chunks per accumulation group
+    const int g = atoi(e);
+    if (g >= 1 && nk % g == 0) a.G = g;
+  }
   const int64_t n_ct = (n + BN - 1) / BN;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -682,6 +700,7 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
   auto kern = bps_tc_kernel<F32, TRANS, NMT, BN_>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
   if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+#ifdef BPS_TC_INSTRUMENT
   if (a.dbg & 8) {  // debug trace: per-CTA cycle counters, printed to stderr (synchronises)
     cudaMalloc(&a.trace, (size_t)grid * 16 * 8);
     cudaMemsetAsync(a.trace, 0, (size_t)grid * 16 * 8, st);
@@ -705,6 +724,10 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     }
     cudaFree(a.trace);
   }
+#else
+  kern<<<(unsigned)grid, K::NTHREADS, K::SMEM, st>>>(tm, a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+#endif
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("bps_tc_kernel launch: ") + cudaGetErrorString(e));
   return BPS_OK;

@@ -1,6 +1,7 @@
 """Run one traced apply (BPS_TC_DEBUG=8) per config and print the per-role cycle breakdown."""
 import os, sys
 os.environ["BPS_TC_DEBUG"] = os.environ.get("BPS_TC_DEBUG", "8")
+os.environ.setdefault("BPS_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2602_06071_b200", "libbps_instr.so"))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth
 from paper_2602_06071_b200 import Sketch, configs as C
