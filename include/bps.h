@@ -114,6 +114,24 @@ int bps_apply_t_ex(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, 
                    float* Yt, int64_t ldyt, void* stream, int variant);
 
 /*
+ * Workspace forms.  With a device workspace of at least bps_workspace_size() bytes the tc
+ *   variant splits the input stream into equal stage-granular ranges (one per SM) instead of
+ *   whole-block ranges; outputs split between ranges are accumulated into Y and into the
+ *   workspace by range parity (each buffer gets ≤ 2 addends per element, so the result is
+ *   still bitwise reproducible) and a final pass adds the workspace into Y.  Without a
+ *   (large enough) workspace these calls behave like bps_apply / bps_apply_t.
+ *   The workspace is caller-owned device memory, 16-byte aligned, not overlapping Y; its
+ *   contents are scratch.  bytes = 0 means no workspace is useful for this shape/dtype.
+ */
+int bps_workspace_size(const bps_sketch* sk, int64_t n, bps_dtype dtype, int transposed, size_t* bytes);
+int bps_apply_ws(const bps_sketch* sk, const void* A, int64_t lda, int64_t n, bps_dtype dtype,
+                 float* Y, int64_t ldy, void* workspace, size_t workspace_bytes, void* stream,
+                 int variant);
+int bps_apply_t_ws(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, bps_dtype dtype,
+                   float* Yt, int64_t ldyt, void* workspace, size_t workspace_bytes, void* stream,
+                   int variant);
+
+/*
  * bps_orbit — the wiring orbit g_pos = f^pos(0), pos = 0..M-1 (host).
  *   With this ordering N(g_i) = (g_{i+1}, ..., g_{i+κ}) (indices mod M), which is what
  *   makes block sharding contiguous.  g_of_pos: host array of length M.

@@ -21,7 +21,7 @@ STATUS = {
 }
 EXPORTS = [
     "bps_make_sketch", "bps_free_sketch", "bps_sketch_info", "bps_apply", "bps_apply_t", "bps_apply_ex",
-    "bps_apply_t_ex", "bps_orbit", "bps_apply_orbit_range", "bps_pattern_host", "bps_kernel_launches", "bps_version", "bps_last_error",
+    "bps_apply_t_ex", "bps_workspace_size", "bps_apply_ws", "bps_apply_t_ws", "bps_orbit", "bps_apply_orbit_range", "bps_pattern_host", "bps_kernel_launches", "bps_version", "bps_last_error",
 ]
 
 
@@ -52,6 +52,12 @@ def _load() -> ctypes.CDLL:
     for name in ("bps_apply_ex", "bps_apply_t_ex"):
         f = getattr(L, name)
         f.argtypes = [vp, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_int]
+        f.restype = ctypes.c_int
+    L.bps_workspace_size.argtypes = [vp, i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]
+    L.bps_workspace_size.restype = ctypes.c_int
+    for name in ("bps_apply_ws", "bps_apply_t_ws"):
+        f = getattr(L, name)
+        f.argtypes = [vp, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_size_t, vp, ctypes.c_int]
         f.restype = ctypes.c_int
     L.bps_orbit.argtypes = [vp, ctypes.POINTER(i32)]
     L.bps_orbit.restype = ctypes.c_int

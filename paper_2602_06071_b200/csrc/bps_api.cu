@@ -112,13 +112,15 @@ static int validate_apply(const bps_sketch* sk, const void* in, int64_t ldin, in
 }
 
 static int dispatch(const bps_sketch* sk, const void* in, int64_t ldin, int64_t n, bps_dtype dt, float* out,
-                    int64_t ldout, bool transposed, const Placement& pl, void* stream, int variant) {
+                    int64_t ldout, bool transposed, const Placement& pl, void* stream, int variant,
+                    void* ws = nullptr, size_t ws_bytes = 0) {
   int rc = check_device();
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const bool tc_ok = tc_supported(sk->p, n, dt, transposed, pl) == BPS_OK;
   if (variant == BPS_VARIANT_TC && !tc_ok) return BPS_ERR_UNSUPPORTED;  // message set by tc_supported
-  if (tc_ok && variant != BPS_VARIANT_SPARSE) return launch_tc(sk->p, in, ldin, n, dt, out, ldout, transposed, pl, st);
+  if (tc_ok && variant != BPS_VARIANT_SPARSE)
+    return launch_tc(sk->p, in, ldin, n, dt, out, ldout, transposed, pl, ws, ws_bytes, st);
   return transposed ? launch_sparse_transposed(sk->p, in, ldin, n, dt, out, ldout, pl, st)
                     : launch_sparse_rowmajor(sk->p, in, ldin, n, dt, out, ldout, pl, st);
 }
@@ -226,6 +228,34 @@ int bps_apply_t_ex(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, 
 int bps_apply_t(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, bps_dtype dtype, float* Yt, int64_t ldyt,
                 void* stream) {
   return bps_apply_t_ex(sk, X, ldx, n, dtype, Yt, ldyt, stream, BPS_VARIANT_AUTO);
+}
+
+int bps_workspace_size(const bps_sketch* sk, int64_t n, bps_dtype dtype, int transposed, size_t* bytes) {
+  if (!sk || !bytes) return fail(BPS_ERR_INVALID_ARG, "NULL argument");
+  if (n < 0) return fail(BPS_ERR_INVALID_ARG, "negative n");
+  Placement pl{0, 0, sk->M};
+  *bytes = tc_workspace_bytes(sk->p, n, dtype, transposed != 0, pl);
+  return BPS_OK;
+}
+
+int bps_apply_ws(const bps_sketch* sk, const void* A, int64_t lda, int64_t n, bps_dtype dtype, float* Y, int64_t ldy,
+                 void* workspace, size_t workspace_bytes, void* stream, int variant) {
+  int rc = validate_apply(sk, A, lda, sk ? sk->d : 0, n, dtype, Y, ldy, sk ? sk->k : 0, n, variant);
+  if (rc || n == 0) return rc;
+  if (workspace && overlaps(workspace, workspace_bytes, Y, (size_t)((sk->k - 1) * ldy + n) * 4))
+    return fail(BPS_ERR_INVALID_ARG, "workspace overlaps the output");
+  Placement pl{0, 0, sk->M};
+  return dispatch(sk, A, lda, n, dtype, Y, ldy, false, pl, stream, variant, workspace, workspace_bytes);
+}
+
+int bps_apply_t_ws(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, bps_dtype dtype, float* Yt,
+                   int64_t ldyt, void* workspace, size_t workspace_bytes, void* stream, int variant) {
+  int rc = validate_apply(sk, X, ldx, n, sk ? sk->d : 0, dtype, Yt, ldyt, n, sk ? sk->k : 0, variant);
+  if (rc || n == 0) return rc;
+  if (workspace && overlaps(workspace, workspace_bytes, Yt, (size_t)((n - 1) * ldyt + sk->k) * 4))
+    return fail(BPS_ERR_INVALID_ARG, "workspace overlaps the output");
+  Placement pl{0, 0, sk->M};
+  return dispatch(sk, X, ldx, n, dtype, Yt, ldyt, true, pl, stream, variant, workspace, workspace_bytes);
 }
 
 int bps_apply_orbit_range(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end, const void* A_local, int64_t lda,

@@ -40,7 +40,8 @@ int launch_sparse_transposed(const SketchParams& p, const void* X, int64_t ldx, 
 
 // tcgen05 kernels (bps_tc.cu). Return BPS_ERR_UNSUPPORTED when the shape is not covered.
 int tc_supported(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl);
+size_t tc_workspace_bytes(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl);
 int launch_tc(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt, float* Y, int64_t ldy,
-              bool transposed, const Placement& pl, cudaStream_t st);
+              bool transposed, const Placement& pl, void* ws, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace bps

@@ -91,6 +91,9 @@ struct TcArgs {
   int64_t stream_begin;        // first input position of the launch window
   int64_t stream_len;          // number of input positions in the window
   int R;                       // ranges per column tile
+  int balanced;                // 1: stage-granular equal ranges, split outputs parity-routed to Y / Y2
+  float* Y2;                   // balanced mode: second accumulation buffer (odd ranges), same shape as Y
+  int64_t ldy2;
   int G;                       // K-chunks per accumulation group (divides B_c/64)
   int dbg;  // experiment switches (env BPS_TC_DEBUG; 0 in production): 1 no band, 2 no convert, 4 no MMA,
             // 8 cycle trace, 16 no band proxy fence, 32 band without hashing
@@ -150,9 +153,20 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
   // ---- this CTA's column tile and input-position range
   const int ct = blockIdx.x / args.R, rr = blockIdx.x % args.R;
   const int64_t col0 = (int64_t)ct * BN;
-  const int64_t Lq = args.stream_len / args.R, Lrem = args.stream_len % args.R;
-  const int64_t P = args.stream_begin + rr * Lq + (rr < Lrem ? rr : Lrem);
-  const int64_t L = Lq + (rr < Lrem ? 1 : 0);
+  // stage s ∈ [S0, S1) of the window = K-chunk s % nk of input position sb + s / nk
+  const int64_t sb = args.stream_begin;
+  int64_t S0, S1;
+  if (args.balanced) {
+    const int64_t Ts = args.stream_len * nk;
+    S0 = Ts * rr / args.R;
+    S1 = Ts * (rr + 1) / args.R;
+  } else {
+    const int64_t Lq = args.stream_len / args.R, Lrem = args.stream_len % args.R;
+    S0 = (rr * Lq + (rr < Lrem ? rr : Lrem)) * nk;
+    S1 = S0 + (Lq + (rr < Lrem ? 1 : 0)) * nk;
+  }
+  float* const Ysplit = (args.balanced && (rr & 1)) ? args.Y2 : args.Y;  // destination of split outputs
+  const int64_t ldsplit = (args.balanced && (rr & 1)) ? args.ldy2 : args.ldy;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < K::NRAW; ++i) {
@@ -176,19 +190,21 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
   const uint32_t tmem = *tmem_ptr;               // D: per-group tensor-core accumulator
   const uint32_t tmem_S = tmem + NMT * K::DN;    // S: fp32 running sums (RN adds on CUDA cores)
 
-  if (L > 0) {
+  if (S1 > S0) {
     if (warp == K::W_TMA) {
       // ===================== TMA producer =====================
       if (lane == 0) {
         const Tr tr(args.trace ? args.trace + blockIdx.x * 16 : nullptr);
         const unsigned long long tstart = tr.now();
         const uint64_t pol = ptx::policy_evict_first();
-        uint32_t gq = affine_pow(p, (uint64_t)mod_pos(P, p.M), 0u);
+        int64_t q = sb + S0 / nk;
+        int kc = (int)(S0 % nk);
+        uint32_t gq = affine_pow(p, (uint64_t)mod_pos(q, p.M), 0u);
         int s = 0;
         uint32_t ph = 0;
-        for (int64_t q = P; q < P + L; ++q) {
-          const int64_t row0 = args.range_mode ? (q - (args.pos_begin + 1)) * (int64_t)p.B_c : (int64_t)gq * p.B_c;
-          for (int kc = 0; kc < nk; ++kc) {
+        for (int64_t st = S0; st < S1; ++st) {
+          {
+            const int64_t row0 = args.range_mode ? (q - (args.pos_begin + 1)) * (int64_t)p.B_c : (int64_t)gq * p.B_c;
             const unsigned long long t0 = tr.now();
             ptx::mbar_wait_sleep(&raw_empty[s], ph ^ 1, 20);
             tr.add(0, t0);
@@ -208,7 +224,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
             }
             if (++s == K::NRAW) s = 0, ph ^= 1;
           }
-          gq = affine_step(p, gq);
+          if (++kc == nk) kc = 0, ++q, gq = affine_step(p, gq);
         }
         tr.add(1, tstart);
       }
@@ -226,10 +242,12 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         constexpr int DSTAGE = K::RAW_STAGE;
         const uint32_t band_base = ptx::smem_u32(smem + K::OFF_BAND);
         bool first_group = true;
-        for (int64_t q = P; q < P + L; ++q) {
-          for (int kc = 0; kc < nk; ++kc) {
-            const int gi = kc % G;
-            if (gi == 0 && !first_group) {  // D must have been folded into S
+        int kc = (int)(S0 % nk);
+        for (int64_t st = S0; st < S1; ++st, kc = (kc + 1 == nk) ? 0 : kc + 1) {
+          {
+            const bool gstart = st == S0 || kc == 0 || kc % G == 0;
+            const bool gend = st == S1 - 1 || kc == nk - 1 || kc % G == G - 1;
+            if (gstart && !first_group) {  // D must have been folded into S
               const unsigned long long t0 = tr.now();
               ptx::mbar_wait(acc_free, fph);
               tr.add(2, t0);
@@ -252,7 +270,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
                 const uint64_t adesc = ptx::smem_desc_sw128(bbase + m * kBandTile + ks * 32, 0, 1024);
                 const uint64_t bdesc = TRANS ? ptx::smem_desc_sw128(dbase + ks * 32, 0, 1024)
                                              : ptx::smem_desc_sw128(dbase + ks * 16 * 128, kBK * 128, 1024);
-                const uint32_t acc = (gi == 0 && ks == 0) ? 0u : 1u;  // fresh per group
+                const uint32_t acc = (gstart && ks == 0) ? 0u : 1u;  // fresh per group
                 if (!BPS_DBG(4)) ptx::mma_bf16_ss(tmem + m * K::DN, adesc, bdesc, K::IDESC, acc);
               }
             }
@@ -260,7 +278,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
             ptx::mma_commit(&band_empty[bs]);
             if (++ds == NDS) ds = 0, dph ^= 1;
             if (++bs == K::NBAND) bs = 0, bph ^= 1;
-            if (gi == G - 1) {
+            if (gend) {
               ptx::mma_commit(acc_full);
               first_group = false;
             }
@@ -284,13 +302,16 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         const bool owned = args.range_mode ? (i >= args.pos_begin && i < args.pos_end) : true;
         if (!owned) return;
         const uint32_t lo = mod_pos(i, kappa) * p.B_r;
-        const bool complete = (i + 1 >= P) && (i + (int64_t)kappa <= P + L - 1);
+        // complete iff every stage of input blocks i+1 .. i+κ lies in this CTA's range
+        const bool complete = (i + 1 - sb) * nk >= S0 && (i + (int64_t)kappa + 1 - sb) * nk <= S1;
         const int64_t row = (args.range_mode ? (i - args.pos_begin) * (int64_t)p.B_r
                                              : (int64_t)affine_pow(p, (uint64_t)mod_pos(i, p.M), 0u) * p.B_r) +
                             (int64_t)(rho - lo);
         const int64_t cbase = col0 + c0;
+        float* const Yd = complete ? args.Y : Ysplit;
+        const int64_t ldd = complete ? args.ldy : ldsplit;
         if (!TRANS) {
-          float* y = args.Y + row * args.ldy + cbase;
+          float* y = Yd + row * ldd + cbase;
 #pragma unroll
           for (int t = 0; t < 16; t += 4) {
             const float a0 = vals[t] * p.scale, a1 = vals[t + 1] * p.scale;
@@ -311,7 +332,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
             if (cbase + t < args.n) {
-              float* y = args.Y + (cbase + t) * args.ldy + row;
+              float* y = Yd + (cbase + t) * ldd + row;
               const float a = vals[t] * p.scale;
               if (complete) *y = a;
               else ptx::red_add(y, a);
@@ -320,19 +341,22 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         }
       };
       uint32_t aph = 0;
-      const int ngrp = nk / G;
       const Tr tr((args.trace && threadIdx.x == 0) ? args.trace + blockIdx.x * 16 : nullptr);
       const unsigned long long tstart = tr.now();
-      for (int64_t q = P; q < P + L; ++q) {
-        const int64_t i = q - (int64_t)kappa;  // output completed by input block q
+      int kc = (int)(S0 % nk);
+      int64_t q = sb + S0 / nk;
+      for (int64_t st = S0; st < S1; ++st, q += (kc + 1 == nk), kc = (kc + 1 == nk) ? 0 : kc + 1) {
+        const bool gend = st == S1 - 1 || kc == nk - 1 || kc % G == G - 1;
+        if (!gend) continue;
+        const int64_t i = q - (int64_t)kappa;  // output completed by input block q (if q ends here)
         const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
-        for (int gix = 0; gix < ngrp; ++gix) {
+        {
           const unsigned long long t0 = tr.now();
           ptx::mbar_wait_sleep(acc_full, aph, 32);
           tr.add(9, t0);
           aph ^= 1;
           ptx::tc_fence_after();
-          const bool last = gix == ngrp - 1;
+          const bool last = kc == nk - 1;  // input block q fully streamed: output q-κ is done here
 #pragma unroll 1
           for (int m = 0; m < NMT; ++m) {
             const uint32_t rho = m * 128 + qtr * 32 + lane;
@@ -367,8 +391,10 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         }
       }
       tr.add(10, tstart);
-      // range end: outputs P+L-κ .. P+L-2 hold partial sums in S
-      for (int64_t i = P + L - (int64_t)kappa; i <= P + L - 2; ++i) {
+      // range end: outputs fed by the last input block that are still open hold partial sums in S
+      const int64_t q_last = sb + (S1 - 1) / nk;
+      const bool full_end = (S1 - 1) % nk == nk - 1;
+      for (int64_t i = q_last - (int64_t)kappa + (full_end ? 1 : 0); i <= q_last - 1; ++i) {
         const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
 #pragma unroll 1
         for (int m = 0; m < NMT; ++m) {
@@ -420,15 +446,17 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
       int64_t stage_no = 0;
       const Tr tr((args.trace && bt == 0) ? args.trace + blockIdx.x * 16 : nullptr);
       const unsigned long long tstart = tr.now();
-      for (int64_t q = P; q < P + L; ++q) {
+      int kc = (int)(S0 % nk);
+      int64_t q = sb + S0 / nk;
+      for (int64_t st = S0; st < S1; ++st, q += (kc + 1 == nk), kc = (kc + 1 == nk) ? 0 : kc + 1, ++stage_no) {
         const int par = (int)(q & 1);  // tables double-buffered by block parity
         uint64_t* ck = ckey + par * 256;
-        for (int kc = 0; kc < nk; ++kc, ++stage_no) {
+        {
           unsigned long long t0 = tr.now();
           ptx::mbar_wait_sleep(&band_empty[bs], bph ^ 1, 20);
           tr.add(6, t0);
           t0 = tr.now();
-          if (kc == 0) {
+          if (kc == 0 || st == S0) {
             // per input block q: hash key of chunk (σ, j): the output i ≡ σ (mod κ) fed by q is
             // i = q - ℓ with ℓ = ((q - σ - 1) mod κ) + 1
             for (uint32_t c = bt; c < ncombo; c += K::NBANDT) {
@@ -511,7 +539,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
       (void)off_odd;
       int rs = 0;
       uint32_t rph = 0;
-      const int64_t total = L * nk;
+      const int64_t total = S1 - S0;
       const Tr tr((args.trace && cv == 0) ? args.trace + blockIdx.x * 16 : nullptr);
       const unsigned long long tstart = tr.now();
       for (int64_t it = 0; it < total; ++it) {
@@ -549,6 +577,26 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
   if (warp == K::W_MMA) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, K::TMEM_COLS);
+  }
+}
+
+// Y += Y2 (balanced decomposition: the two parity buffers of split outputs; a fixed-order,
+// deterministic final combine).
+__global__ void __launch_bounds__(256) bps_add_kernel(float* __restrict__ Y, int64_t ldy, const float* __restrict__ Y2,
+                                                      int64_t ldy2, int64_t rows, int64_t cols) {
+  const int64_t c4 = (cols + 3) / 4;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * c4; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / c4, c = (e % c4) * 4;
+    float* y = Y + r * ldy + c;
+    const float* z = Y2 + r * ldy2 + c;
+    if (c + 4 <= cols) {
+      float4 a = *reinterpret_cast<float4*>(y);
+      const float4 b = *reinterpret_cast<const float4*>(z);
+      a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+      *reinterpret_cast<float4*>(y) = a;
+    } else {
+      for (int64_t t = c; t < cols; ++t) Y[r * ldy + t] += Y2[r * ldy2 + t];
+    }
   }
 }
 
@@ -614,7 +662,7 @@ int64_t ranges_for(const SketchParams& p, int64_t stream_len, int64_t n_ct, int 
 
 template <bool F32, bool TRANS, int NMT, int BN_>
 int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, float* Y, int64_t ldy,
-                const Placement& pl, cudaStream_t st) {
+                const Placement& pl, float* Y2, int64_t ldy2, cudaStream_t st) {
   using K = Cfg<F32, TRANS, NMT, BN_>;
   constexpr int BN = K::BN;
   EncodeTiledFn enc = encode_fn();
@@ -662,7 +710,20 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t R = ranges_for(p, a.stream_len, n_ct, sms);
+  int64_t R;
+  a.balanced = Y2 != nullptr;
+  a.Y2 = Y2;
+  a.ldy2 = ldy2;
+  if (a.balanced) {
+    // stage-granular equal ranges: every range ≥ (κ·nk − 1)/3 stages, so an output window of
+    // κ·nk stages meets ≤ 4 ranges and each parity buffer receives ≤ 2 addends per element
+    const int64_t Ts = a.stream_len * nk, W = (int64_t)p.kappa * nk;
+    R = n_ct >= sms ? 1 : sms / n_ct;
+    if (R > Ts) R = Ts;
+    while (R > 1 && Ts / R < (W - 1 + 2) / 3) --R;
+  } else {
+    R = ranges_for(p, a.stream_len, n_ct, sms);
+  }
   a.R = (int)R;
   const int64_t grid = n_ct * R;
   if (grid > 0x7FFFFFFF) return fail(BPS_ERR_UNSUPPORTED, "grid too large");
@@ -690,11 +751,12 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(BPS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
 
-  // outputs split between two CTAs are accumulated with red.add into a zeroed Y
-  if (p.kappa > 1) {
-    const int64_t krows = pl.range_mode ? pl.n_out * (int64_t)p.B_r : (int64_t)p.M * p.B_r;
-    cudaError_t e = TRANS ? cudaMemset2DAsync(Y, ldy * 4, 0, (size_t)krows * 4, (size_t)n, st)
-                          : cudaMemset2DAsync(Y, ldy * 4, 0, (size_t)n * 4, (size_t)krows, st);
+  // outputs split between CTAs are accumulated with red.add into zeroed buffers
+  const int64_t krows = pl.range_mode ? pl.n_out * (int64_t)p.B_r : (int64_t)p.M * p.B_r;
+  const int64_t yrows = TRANS ? n : krows, ycols = TRANS ? krows : n;
+  if (p.kappa > 1 || a.balanced) {
+    cudaError_t e = cudaMemset2DAsync(Y, ldy * 4, 0, (size_t)ycols * 4, (size_t)yrows, st);
+    if (e == cudaSuccess && a.balanced) e = cudaMemset2DAsync(Y2, ldy2 * 4, 0, (size_t)ycols * 4, (size_t)yrows, st);
     if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaMemset2DAsync: ") + cudaGetErrorString(e));
   }
   auto kern = bps_tc_kernel<F32, TRANS, NMT, BN_>;
@@ -730,6 +792,14 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
 #endif
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("bps_tc_kernel launch: ") + cudaGetErrorString(e));
+  if (a.balanced) {
+    const int64_t work = yrows * ((ycols + 3) / 4);
+    const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)sms * 8);
+    bps_add_kernel<<<blocks, 256, 0, st>>>(Y, ldy, Y2, ldy2, yrows, ycols);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("bps_add_kernel launch: ") + cudaGetErrorString(e));
+  }
   return BPS_OK;
 }
 
@@ -744,8 +814,23 @@ int tc_supported(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed
   return BPS_OK;
 }
 
+size_t tc_workspace_bytes(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl) {
+  if (!plan_for(p, dt).ok) return 0;
+  const int64_t krows = pl.range_mode ? pl.n_out * (int64_t)p.B_r : (int64_t)p.M * p.B_r;
+  const int64_t rows = transposed ? n : krows, cols = transposed ? krows : n;
+  return (size_t)rows * (size_t)((cols + 3) / 4 * 4) * 4;
+}
+
 int launch_tc(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt, float* Y, int64_t ldy,
-              bool transposed, const Placement& pl, cudaStream_t st) {
+              bool transposed, const Placement& pl, void* ws, size_t ws_bytes, cudaStream_t st) {
+  float* Y2 = nullptr;
+  int64_t ldy2 = 0;
+  const size_t need = tc_workspace_bytes(p, n, dt, transposed, pl);
+  if (ws && need && ws_bytes >= need && ((uintptr_t)ws % 16) == 0) {
+    const int64_t krows = pl.range_mode ? pl.n_out * (int64_t)p.B_r : (int64_t)p.M * p.B_r;
+    Y2 = (float*)ws;
+    ldy2 = ((transposed ? krows : n) + 3) / 4 * 4;
+  }
   Plan plan = plan_for(p, dt);
   if (!plan.ok) return fail(BPS_ERR_UNSUPPORTED, plan.why);
   const bool f32 = dt == BPS_F32;
@@ -764,7 +849,7 @@ int launch_tc(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_
   }
 #define BPS_TC_CASE(F, T, NM, B)                                        \
   if (f32 == F && transposed == T && plan.nmt == NM && bn == B)         \
-    return launch_impl<F, T, NM, B>(p, A, lda, n, Y, ldy, pl, st);
+    return launch_impl<F, T, NM, B>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st);
   BPS_TC_CASE(true, false, 1, 128)
   BPS_TC_CASE(true, true, 1, 128)
   if (f32) bn = 64;

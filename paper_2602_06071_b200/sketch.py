@@ -68,13 +68,31 @@ class Sketch:
         check(lib.bps_orbit(self._h, arr))
         return list(arr)
 
+    def workspace_bytes(self, n: int, dtype_code: int, transposed: bool = False) -> int:
+        key = (n, dtype_code, transposed)
+        cache = self.__dict__.setdefault("_ws_cache", {})
+        if key not in cache:
+            b = ctypes.c_size_t()
+            check(lib.bps_workspace_size(self._h, n, dtype_code, int(transposed), ctypes.byref(b)))
+            cache[key] = b.value
+        return cache[key]
+
+    def _workspace(self, n, dtype_code, transposed, device, use_workspace):
+        """Scratch for the balanced tc decomposition, from torch's caching allocator."""
+        import torch
+
+        nbytes = self.workspace_bytes(n, dtype_code, transposed) if use_workspace else 0
+        if not nbytes:
+            return None, 0
+        return torch.empty(nbytes, dtype=torch.uint8, device=device), nbytes
+
     def pattern(self, g: int, ell: int, u: int, j: int) -> tuple[int, int]:
         r, sg = ctypes.c_int32(), ctypes.c_int32()
         check(lib.bps_pattern_host(self._h, g, ell, u, j, ctypes.byref(r), ctypes.byref(sg)))
         return r.value, sg.value
 
     # ------------------------------------------------------------------ apply
-    def apply(self, A, out=None, variant: str = "auto"):
+    def apply(self, A, out=None, variant: str = "auto", use_workspace: bool = True):
         """Y = S·A. A: cuda d×n (float32/bfloat16, row-major, lda = A.stride(0)) -> k×n float32."""
         import torch
 
@@ -87,11 +105,14 @@ class Sketch:
         _check_matrix(out, "out")
         if out.dtype != torch.float32 or tuple(out.shape) != (self.k, n):
             raise ValueError("out must be float32 k×n")
-        check(lib.bps_apply_ex(self._h, A.data_ptr(), A.stride(0), n, _dtype_code(A), out.data_ptr(), out.stride(0),
-                               _stream_ptr(A.device), VARIANTS[variant]))
+        code = _dtype_code(A)
+        ws, nbytes = self._workspace(n, code, False, A.device, use_workspace)
+        check(lib.bps_apply_ws(self._h, A.data_ptr(), A.stride(0), n, code, out.data_ptr(), out.stride(0),
+                               ws.data_ptr() if ws is not None else None, nbytes, _stream_ptr(A.device),
+                               VARIANTS[variant]))
         return out
 
-    def apply_t(self, X, out=None, variant: str = "auto"):
+    def apply_t(self, X, out=None, variant: str = "auto", use_workspace: bool = True):
         """Transposed layout: X cuda n×d -> (S·Xᵀ)ᵀ, n×k float32."""
         import torch
 
@@ -104,8 +125,11 @@ class Sketch:
         _check_matrix(out, "out")
         if out.dtype != torch.float32 or tuple(out.shape) != (n, self.k):
             raise ValueError("out must be float32 n×k")
-        check(lib.bps_apply_t_ex(self._h, X.data_ptr(), X.stride(0), n, _dtype_code(X), out.data_ptr(), out.stride(0),
-                                 _stream_ptr(X.device), VARIANTS[variant]))
+        code = _dtype_code(X)
+        ws, nbytes = self._workspace(n, code, True, X.device, use_workspace)
+        check(lib.bps_apply_t_ws(self._h, X.data_ptr(), X.stride(0), n, code, out.data_ptr(), out.stride(0),
+                                 ws.data_ptr() if ws is not None else None, nbytes, _stream_ptr(X.device),
+                                 VARIANTS[variant]))
         return out
 
     def apply_orbit_range(self, pos_begin: int, pos_end: int, A_local, out=None, variant: str = "auto"):

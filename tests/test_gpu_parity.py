@@ -236,3 +236,36 @@ def test_grad_config_sampled(variant):
                          ids=lambda c: c.name)
 def test_sweep_sampled(cfg):
     _sampled_check(cfg, "auto")
+
+
+# ------------------------------------- balanced (workspace) vs block-aligned decomposition
+@pytest.mark.parametrize("layout,n,dt", [((128, 32, 8192, 4, 4), 512, "f32"), ((16, 32, 1024, 4, 4), 200, "f32"),
+                                         ((64, 16, 512, 8, 2), 300, "bf16"), ((16, 16, 256, 1, 4), 64, "f32"),
+                                         ((8, 32, 128, 8, 2), 33, "bf16")])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_balanced_decomposition(layout, n, dt, transposed):
+    """Stage-granular ranges with the parity workspace (bps_apply_ws) agree with the oracle and
+    are bitwise reproducible; the block-aligned path (no workspace) agrees too."""
+    sk, osk = _pair(*layout, seed=17)
+    tdt = torch.float32 if dt == "f32" else torch.bfloat16
+    A = synth.host_matrix("gaussian", sk.d, n, seed=4)
+    if dt == "bf16":
+        A = synth.bf16_round(A)
+    ref = oracle.apply(osk, A)
+    nrm = np.linalg.norm(A.astype(np.float64), axis=0)
+    At = torch.from_numpy(np.ascontiguousarray(A.T if transposed else A)).cuda().to(tdt)
+    f = sk.apply_t if transposed else sk.apply
+    outs = []
+    for use_ws in (True, True, False):
+        try:
+            Y = f(At, variant="tc", use_workspace=use_ws)
+        except BpsError as e:
+            if e.code == -3:
+                pytest.skip(str(e))
+            raise
+        torch.cuda.synchronize()
+        Yn = Y.cpu().numpy()
+        outs.append(Yn.T if transposed else Yn)
+    assert np.array_equal(outs[0], outs[1])  # bitwise reproducible
+    for Y in outs:
+        assert_f32(Y, ref, nrm, f"{layout} n={n} {dt} T={transposed}")
