@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--shard", default="column", choices=["column", "block"],
                     help="column: weak scaling, every rank its own n-column batch (no collective); "
                          "block: strong scaling of one d×n problem sharded along the wiring orbit + all-gather")
+    ap.add_argument("--no-workspace", action="store_true", help="block-aligned ranges (no balanced workspace)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -208,7 +209,7 @@ def main():
         Y = torch.empty((cfg.k, n), dtype=torch.float32, device=dev)
 
         def step():
-            sk.apply(A, out=Y, variant=args.variant)
+            sk.apply(A, out=Y, variant=args.variant, use_workspace=not args.no_workspace)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -257,7 +258,7 @@ def main():
 
         def e2e_step():
             A_d.copy_(A_h, non_blocking=True)
-            sk.apply(A_d, out=Y_d, variant=args.variant)
+            sk.apply(A_d, out=Y_d, variant=args.variant, use_workspace=not args.no_workspace)
             Y_h.copy_(Y_d, non_blocking=True)
 
         e2e_step()

@@ -243,10 +243,11 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
         const uint32_t band_base = ptx::smem_u32(smem + K::OFF_BAND);
         bool first_group = true;
         int kc = (int)(S0 % nk);
-        for (int64_t st = S0; st < S1; ++st, kc = (kc + 1 == nk) ? 0 : kc + 1) {
+        int gi = kc % G;  // position inside the accumulation group (groups restart at block starts)
+        for (int64_t st = S0; st < S1; ++st) {
           {
-            const bool gstart = st == S0 || kc == 0 || kc % G == 0;
-            const bool gend = st == S1 - 1 || kc == nk - 1 || kc % G == G - 1;
+            const bool gstart = st == S0 || gi == 0;
+            const bool gend = st == S1 - 1 || kc == nk - 1 || gi == G - 1;
             if (gstart && !first_group) {  // D must have been folded into S
               const unsigned long long t0 = tr.now();
               ptx::mbar_wait(acc_free, fph);
@@ -283,6 +284,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
               first_group = false;
             }
           }
+          if (++kc == nk) kc = 0, gi = 0;
+          else gi = (gi + 1 == G) ? 0 : gi + 1;
         }
         tr.add(5, tstart);
       }
@@ -344,9 +347,11 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_>::NTHREADS, 1)
       const Tr tr((args.trace && threadIdx.x == 0) ? args.trace + blockIdx.x * 16 : nullptr);
       const unsigned long long tstart = tr.now();
       int kc = (int)(S0 % nk);
+      int gi = kc % G;
       int64_t q = sb + S0 / nk;
-      for (int64_t st = S0; st < S1; ++st, q += (kc + 1 == nk), kc = (kc + 1 == nk) ? 0 : kc + 1) {
-        const bool gend = st == S1 - 1 || kc == nk - 1 || kc % G == G - 1;
+      for (int64_t st = S0; st < S1;
+           ++st, q += (kc + 1 == nk), gi = (kc + 1 == nk || gi + 1 == G) ? 0 : gi + 1, kc = (kc + 1 == nk) ? 0 : kc + 1) {
+        const bool gend = st == S1 - 1 || kc == nk - 1 || gi == G - 1;
         if (!gend) continue;
         const int64_t i = q - (int64_t)kappa;  // output completed by input block q (if q ends here)
         const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
