@@ -53,12 +53,13 @@ def _load() -> ctypes.CDLL:
         f = getattr(L, name)
         f.argtypes = [vp, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_int]
         f.restype = ctypes.c_int
-    L.bps_workspace_size.argtypes = [vp, i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]
-    L.bps_workspace_size.restype = ctypes.c_int
-    for name in ("bps_apply_ws", "bps_apply_t_ws"):
-        f = getattr(L, name)
-        f.argtypes = [vp, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_size_t, vp, ctypes.c_int]
-        f.restype = ctypes.c_int
+    if hasattr(L, "bps_workspace_size"):  # absent only in old builds loaded via BPS_LIB for A/B runs
+        L.bps_workspace_size.argtypes = [vp, i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]
+        L.bps_workspace_size.restype = ctypes.c_int
+        for name in ("bps_apply_ws", "bps_apply_t_ws"):
+            f = getattr(L, name)
+            f.argtypes = [vp, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_size_t, vp, ctypes.c_int]
+            f.restype = ctypes.c_int
     L.bps_orbit.argtypes = [vp, ctypes.POINTER(i32)]
     L.bps_orbit.restype = ctypes.c_int
     L.bps_apply_orbit_range.argtypes = [vp, i64, i64, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_int]

@@ -831,7 +831,22 @@ int launch_tc(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_
   float* Y2 = nullptr;
   int64_t ldy2 = 0;
   const size_t need = tc_workspace_bytes(p, n, dt, transposed, pl);
-  if (ws && need && ws_bytes >= need && ((uintptr_t)ws % 16) == 0) {
+  // the balanced decomposition only pays when whole-block ranges are uneven (e.g. LS: 128 blocks
+  // over 37 ranges = 3 or 4 blocks); it costs two memsets and an add pass otherwise
+  bool uneven = false;
+  if (ws) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const Plan pln = plan_for(p, dt);
+    const int bnx = (dt == BPS_F32) ? (pln.nmt == 1 ? 128 : 64) : 128;  // conservative (smaller) tile
+    const int64_t sl = pl.range_mode ? pl.n_out + p.kappa - 1 : (int64_t)p.M;
+    const int64_t nct = (n + bnx - 1) / bnx;
+    const int64_t R = ranges_for(p, sl, nct, sms);
+    const int64_t Lmax = (sl + R - 1) / R;
+    uneven = R > 1 && (double)Lmax * R > 1.05 * (double)sl;
+  }
+  if (ws && uneven && need && ws_bytes >= need && ((uintptr_t)ws % 16) == 0) {
     const int64_t krows = pl.range_mode ? pl.n_out * (int64_t)p.B_r : (int64_t)p.M * p.B_r;
     Y2 = (float*)ws;
     ldy2 = ((transposed ? krows : n) + 3) / 4 * 4;

@@ -81,7 +81,7 @@ class Sketch:
         """Scratch for the balanced tc decomposition, from torch's caching allocator."""
         import torch
 
-        nbytes = self.workspace_bytes(n, dtype_code, transposed) if use_workspace else 0
+        nbytes = self.workspace_bytes(n, dtype_code, transposed) if use_workspace and hasattr(lib, "bps_workspace_size") else 0
         if not nbytes:
             return None, 0
         return torch.empty(nbytes, dtype=torch.uint8, device=device), nbytes
@@ -107,6 +107,10 @@ class Sketch:
             raise ValueError("out must be float32 k×n")
         code = _dtype_code(A)
         ws, nbytes = self._workspace(n, code, False, A.device, use_workspace)
+        if ws is None:
+            check(lib.bps_apply_ex(self._h, A.data_ptr(), A.stride(0), n, code, out.data_ptr(), out.stride(0),
+                                   _stream_ptr(A.device), VARIANTS[variant]))
+            return out
         check(lib.bps_apply_ws(self._h, A.data_ptr(), A.stride(0), n, code, out.data_ptr(), out.stride(0),
                                ws.data_ptr() if ws is not None else None, nbytes, _stream_ptr(A.device),
                                VARIANTS[variant]))
@@ -127,6 +131,10 @@ class Sketch:
             raise ValueError("out must be float32 n×k")
         code = _dtype_code(X)
         ws, nbytes = self._workspace(n, code, True, X.device, use_workspace)
+        if ws is None:
+            check(lib.bps_apply_t_ex(self._h, X.data_ptr(), X.stride(0), n, code, out.data_ptr(), out.stride(0),
+                                     _stream_ptr(X.device), VARIANTS[variant]))
+            return out
         check(lib.bps_apply_t_ws(self._h, X.data_ptr(), X.stride(0), n, code, out.data_ptr(), out.stride(0),
                                  ws.data_ptr() if ws is not None else None, nbytes, _stream_ptr(X.device),
                                  VARIANTS[variant]))
