@@ -44,12 +44,14 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False, instrument: bool = False) -> str:
-    out = LIB_INSTR if instrument else LIB
-    if not force and not instrument and not needs_build():
+def build(force: bool = False, verbose: bool = False, instrument: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    custom = out is not None
+    out = out or (LIB_INSTR if instrument else LIB)
+    if not force and not instrument and not custom and not needs_build():
         return LIB
     tmp = out + ".tmp"
-    extra = ["-DBPS_TC_INSTRUMENT"] if instrument else []
+    extra = (["-DBPS_TC_INSTRUMENT"] if instrument else []) + [f"-D{d}" for d in defines]
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(HERE, "..", "include"), "-o", tmp, *sources()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
@@ -65,4 +67,7 @@ def build(force: bool = False, verbose: bool = False, instrument: bool = False) 
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, instrument="--instrument" in sys.argv))
+    args = sys.argv[1:]
+    out = next((a.split("=", 1)[1] for a in args if a.startswith("--out=")), None)
+    defs = tuple(a[2:] for a in args if a.startswith("-D"))
+    print(build(force="--force" in args, verbose="-v" in args, instrument="--instrument" in args, out=out, defines=defs))

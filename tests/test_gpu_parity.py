@@ -240,7 +240,7 @@ def test_sweep_sampled(cfg):
 
 # ------------------------------------- balanced (workspace) vs block-aligned decomposition
 @pytest.mark.parametrize("layout,n,dt", [((128, 32, 8192, 4, 4), 512, "f32"), ((16, 32, 1024, 4, 4), 200, "f32"),
-                                         ((64, 16, 512, 8, 2), 300, "bf16"), ((16, 16, 256, 1, 4), 64, "f32"),
+                                         ((64, 16, 512, 8, 2), 304, "bf16"), ((16, 16, 256, 1, 4), 64, "f32"),
                                          ((8, 32, 128, 8, 2), 48, "bf16")])
 @pytest.mark.parametrize("transposed", [False, True])
 def test_balanced_decomposition(layout, n, dt, transposed):
