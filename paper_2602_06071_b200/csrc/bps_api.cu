@@ -165,6 +165,7 @@ int bps_make_sketch(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t 
   p.kappa = (uint32_t)kappa;
   p.s = (uint32_t)s;
   p.C = (uint32_t)(B_r / s);
+  p.Mmask = ((M & (M - 1)) == 0) ? (uint32_t)(M - 1) : 0u;
   select_affine(seed, (uint64_t)M, &p.a, &p.b);
   p.K = mix64(seed ^ kTagPhi);
   p.scale = (float)(1.0 / std::sqrt((double)kappa * (double)s));

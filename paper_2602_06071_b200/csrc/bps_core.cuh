@@ -28,6 +28,7 @@ BPS_HD uint64_t mix64(uint64_t z) {
 // Parameters every kernel needs; passed by value (fits in the param space).
 struct SketchParams {
   uint32_t M, B_r, B_c, kappa, s, C;  // C = B_r / s (row-partition chunk, R1)
+  uint32_t Mmask;                     // M-1 if M is a power of two (fast mod), else 0
   uint32_t a, b;                      // f(x) = (a x + b) mod M   (R4)
   uint64_t K;                         // mix64(seed ^ kTagPhi)     (R2)
   float scale;                        // fp32(1/sqrt(kappa*s))     (R6)
@@ -35,11 +36,25 @@ struct SketchParams {
 
 // f(x) = (a x + b) mod M.
 BPS_HD uint32_t affine_step(const SketchParams& p, uint32_t x) {
+  if (p.Mmask) return (p.a * x + p.b) & p.Mmask;  // M = 2^m ≤ 2^24: low 32 bits of a·x+b suffice
   return (uint32_t)(((uint64_t)p.a * x + p.b) % p.M);
 }
 
 // f^e(x) by composing affine maps (square-and-multiply), e ≥ 0.
 BPS_HD uint32_t affine_pow(const SketchParams& p, uint64_t e, uint32_t x) {
+  if (p.Mmask) {  // power-of-two M: all arithmetic mod 2^32 then masked
+    uint32_t ra = 1, rb = 0, ba = p.a, bb = p.b;
+    while (e) {
+      if (e & 1) {
+        rb = ba * rb + bb;
+        ra = ba * ra;
+      }
+      bb = ba * bb + bb;
+      ba = ba * ba;
+      e >>= 1;
+    }
+    return (ra * x + rb) & p.Mmask;
+  }
   // Represent a map as (ma, mb): x -> ma x + mb (mod M).
   uint64_t ra = 1 % p.M, rb = 0;           // accumulated result
   uint64_t ba = p.a % p.M, bb = p.b % p.M; // f^(2^i)
