@@ -21,7 +21,7 @@ if [ -n "$NCU" ]; then
     timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_${c}.csv \
        python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks > /dev/null 2>&1
     echo "ncu launches $c rc=$?"
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:bps_ -s 3 -c 1 -o gpurun_out/prof_${c} -f \
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:bps_tc_kernel -s 3 -c 1 -o gpurun_out/prof_${c} -f \
        python bench.py --config $c --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks > gpurun_out/ncu_full_${c}.log 2>&1
     echo "ncu full $c rc=$?"
   done
