@@ -269,3 +269,14 @@ def test_balanced_decomposition(layout, n, dt, transposed):
     assert np.array_equal(outs[0], outs[1])  # bitwise reproducible
     for Y in outs:
         assert_f32(Y, ref, nrm, f"{layout} n={n} {dt} T={transposed}")
+
+
+def test_scaleout_config_one_panel_sampled():
+    """BASELINE configs[4] (d=2^26, k=16384, κ=8, s=4, bf16) at full d on one column panel
+    (n=512, 64 GiB of A): the per-rank unit of the 8-GPU scale-out run."""
+    cfg = C.SCALEOUT.with_(n=512)
+    free, _ = torch.cuda.mem_get_info()
+    if free < cfg.d * cfg.n * 2 * 1.1:
+        pytest.skip("not enough device memory for one scale-out panel")
+    _sampled_check(cfg, "auto", n_cols=4, n_blocks=2)
+    torch.cuda.empty_cache()
