@@ -51,6 +51,8 @@ class Config:
 TINY = Config("tiny", d=1024, k=256, kappa=2, s=2, n=16, dtype="f32", B_r=32)
 LS = Config("ls", d=1 << 20, k=4096, kappa=4, s=4, n=512, dtype="f32", B_r=32)
 GRAD = Config("grad", d=1 << 24, k=8192, kappa=8, s=2, n=4096, dtype="bf16", B_r=16)
+# narrow inputs (per-example gradient batches, P:1841-1842 low-occupancy case): d large, n small
+SMALLN = Config("smalln", d=1 << 24, k=8192, kappa=8, s=2, n=32, dtype="bf16", B_r=16)
 SCALEOUT = Config("scaleout", d=1 << 26, k=16384, kappa=8, s=4, n=16384, dtype="bf16", B_r=16)
 
 
@@ -59,4 +61,4 @@ def sweep(kappa: int, s: int, dtype: str = "bf16") -> Config:
 
 
 SWEEP = [sweep(k, s, dt) for dt in ("bf16", "f32") for k in (1, 2, 4, 8, 16) for s in (1, 2, 4, 8)]
-CONFIGS = {c.name: c for c in [TINY, LS, GRAD, SCALEOUT] + SWEEP}
+CONFIGS = {c.name: c for c in [TINY, LS, GRAD, SMALLN, SCALEOUT] + SWEEP}
