@@ -28,6 +28,7 @@ from .blockperm import (  # noqa: F401
     TAG_PHI,
     Sketch,
     apply,
+    apply_adjoint,
     apply_t,
     build_S_csr,
     build_S_dense,

@@ -300,6 +300,17 @@ def apply_t(sk: Sketch, X: np.ndarray, blocks=None) -> np.ndarray:
     return apply(sk, X64.T, blocks).T
 
 
+def apply_adjoint(sk: Sketch, Yin: np.ndarray) -> np.ndarray:
+    """X = Sᵀ·Y in float64 (Y: k×n) — the adjoint of the sketch, the plain
+    transpose of the explicit S of P:36-42."""
+    Y64 = np.asarray(Yin, dtype=np.float64)
+    if Y64.shape[0] != sk.k:
+        raise ValueError("Y must have k rows")
+    if sk.k * sk.d <= (1 << 22):
+        return build_S_dense(sk).T @ Y64
+    return build_S_csr(sk).T @ Y64
+
+
 def sketch_rows(sk: Sketch, g: int) -> np.ndarray:
     """Global row indices of output block g (P:1663-1666 tiles)."""
     return np.arange(g * sk.B_r, (g + 1) * sk.B_r)

@@ -235,3 +235,22 @@ def test_matches_independent_scratch_vectors():
         for u, pair in enumerate(t[key]):
             for j, (row, sign) in enumerate(pair):
                 assert bp.pattern(sk, 0, ell, u, j) == (row, sign)
+
+
+def test_adjoint_identity():
+    """⟨S x, y⟩ = ⟨x, Sᵀ y⟩ for all x, y (definition of the adjoint), through the oracle's two
+    independent code paths (apply builds rows of S per output block; apply_adjoint transposes)."""
+    rng = np.random.default_rng(9)
+    for layout in [(8, 32, 128, 2, 2), (16, 64, 128, 4, 2), (32, 16, 256, 8, 2)]:
+        sk = oracle.make_sketch(*layout, seed=4)
+        X = rng.standard_normal((sk.d, 3))
+        Yv = rng.standard_normal((sk.k, 3))
+        lhs = np.sum(oracle.apply(sk, X) * Yv)
+        rhs = np.sum(X * oracle.apply_adjoint(sk, Yv))
+        assert lhs == pytest.approx(rhs, rel=1e-12)
+        # each column of Sᵀ has κs... each row of Sᵀ (= column of S) has κs nonzeros: Sᵀ e_i
+        E = np.zeros((sk.k, 1))
+        E[5] = 1.0
+        col = oracle.apply_adjoint(sk, E)[:, 0]
+        S = oracle.build_S_dense(sk)
+        assert np.array_equal(col, S[5])
