@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--shard", default="column", choices=["column", "block"],
                     help="column: weak scaling, every rank its own n-column batch (no collective); "
                          "block: strong scaling of one d×n problem sharded along the wiring orbit + all-gather")
+    ap.add_argument("--op", default="apply", choices=["apply", "adjoint"],
+                    help="adjoint: X = Sᵀ·Y (fp32 k×n -> d×n) on the same sketch; secondary line, no e2e/cpu legs")
     ap.add_argument("--no-workspace", action="store_true", help="block-aligned ranges (no balanced workspace)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -204,6 +206,13 @@ def main():
 
         def step():
             D.block_sharded_apply(sk, A, out=Y)
+    elif args.op == "adjoint":
+        Yin = synth.device_matrix(args.kind, cfg.k, n, seed=1000 + rank, dtype=torch.float32, device=dev)
+        X = torch.empty((cfg.d, n), dtype=torch.float32, device=dev)
+        args.no_e2e = args.no_cpu_baseline = True
+
+        def step():
+            sk.apply_adjoint(Yin, out=X, variant=args.variant)
     else:
         A = synth.device_matrix(args.kind, cfg.d, n, seed=1000 + rank, M=cfg.M, dtype=tdt, device=dev)
         Y = torch.empty((cfg.k, n), dtype=torch.float32, device=dev)
@@ -241,6 +250,8 @@ def main():
     ms = total_max / args.steps
     block = args.shard == "block" and world > 1
     bytes_rank = cfg.roofline_bytes(n) if not block else cfg.roofline_bytes(n) // world
+    if args.op == "adjoint":  # read Y (k×n fp32) once, write X (d×n fp32) once
+        bytes_rank = (cfg.k + cfg.d) * n * 4
     value = world * bytes_rank / (ms / 1e3) / 1e9
     peak, peak_src = measured_peaks()
     achieved = bytes_rank / (statistics.mean(per) / 1e3) / 1e9
@@ -292,13 +303,13 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if args.op == "apply" else "adjoint_throughput_gbs", "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if block else "weak",
-            "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" else "bf16-in/f32-acc",
+            "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" or args.op == "adjoint" else "bf16-in/f32-acc",
             "data": f"synthetic {args.kind} (torch Philox on device), seed {1000}+rank",
             "config": {"workload": cfg.name, "d": cfg.d, "k": cfg.k, "kappa": cfg.kappa, "s": cfg.s,
-                       "n_per_gpu": n, "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c, "variant": args.variant,
+                       "n_per_gpu": n, "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c, "variant": args.variant, "op": args.op,
                        "parallelism": (f"orbit-block-shard x{world} + NCCL all_gather" if block
                                        else f"column-shard x{world} (no collective)"),
                        "l2": "inputs larger than L2 (no flush needed)" if bytes_rank > (256 << 20) else "input fits L2"},
@@ -307,7 +318,7 @@ def main():
             "frac_of_8tbs": value / world / 8000.0,
             "ms_min": min(per), "ms_median": statistics.median(per),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic(cfg.name, args.variant), "peak_source": peak_src,
+                         "traffic": ncu_traffic(cfg.name, args.variant) if args.op == "apply" else None, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": bytes_rank},
             "gpu_launches": launches,
             "clocks": clk,

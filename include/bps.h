@@ -132,6 +132,24 @@ int bps_apply_t_ws(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, 
                    int variant);
 
 /*
+ * bps_apply_adjoint — X = Sᵀ·Y, the adjoint (transpose) of the same sketch
+ *   (S as in P:36-42 / P:1984-1992; Sᵀ is used e.g. to map a sketched-space solution back,
+ *   SURVEY §8f).  X^(h) = κ^{-1/2} Σ_{g: h∈N(g)} Φ_{g,h}ᵀ Y^(g): row u of input block h gathers
+ *   the κ·s rows of Y named by the column u of the pattern, with the same hash draws (R1-R3).
+ *   Y: device, k × n fp32, row-major, leading dimension ldy (elements).
+ *   X: device, d × n fp32, row-major, ldx; fully overwritten (every element written once, no
+ *      atomics: bitwise reproducible).  Pointers / ld·4 16-byte aligned; X must not overlap Y.
+ *   Kernels: tcgen05 (window of Y as the MMA A operand, the forward's band tile as B) when
+ *   B_c % 64 == 0, κ·s ≤ 64 and κ·B_r ≤ 256; otherwise a CUDA-core gather kernel, which needs
+ *   κ ≤ 64 and κ·B_r ≤ 400, else BPS_ERR_UNSUPPORTED.  n == 0 is a no-op.
+ *   _ex: variant as for bps_apply_ex (TC on an uncovered shape -> BPS_ERR_UNSUPPORTED).
+ */
+int bps_apply_adjoint(const bps_sketch* sk, const float* Y, int64_t ldy, int64_t n, float* X,
+                      int64_t ldx, void* stream);
+int bps_apply_adjoint_ex(const bps_sketch* sk, const float* Y, int64_t ldy, int64_t n, float* X,
+                         int64_t ldx, void* stream, int variant);
+
+/*
  * bps_orbit — the wiring orbit g_pos = f^pos(0), pos = 0..M-1 (host).
  *   With this ordering N(g_i) = (g_{i+1}, ..., g_{i+κ}) (indices mod M), which is what
  *   makes block sharding contiguous.  g_of_pos: host array of length M.

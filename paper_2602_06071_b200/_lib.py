@@ -60,6 +60,10 @@ def _load() -> ctypes.CDLL:
             f = getattr(L, name)
             f.argtypes = [vp, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_size_t, vp, ctypes.c_int]
             f.restype = ctypes.c_int
+    L.bps_apply_adjoint.argtypes = [vp, vp, i64, i64, vp, i64, vp]
+    L.bps_apply_adjoint.restype = ctypes.c_int
+    L.bps_apply_adjoint_ex.argtypes = [vp, vp, i64, i64, vp, i64, vp, ctypes.c_int]
+    L.bps_apply_adjoint_ex.restype = ctypes.c_int
     L.bps_orbit.argtypes = [vp, ctypes.POINTER(i32)]
     L.bps_orbit.restype = ctypes.c_int
     L.bps_apply_orbit_range.argtypes = [vp, i64, i64, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_int]

@@ -259,6 +259,22 @@ int bps_apply_t_ws(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, 
   return dispatch(sk, X, ldx, n, dtype, Yt, ldyt, true, pl, stream, variant, workspace, workspace_bytes);
 }
 
+int bps_apply_adjoint_ex(const bps_sketch* sk, const float* Y, int64_t ldy, int64_t n, float* X, int64_t ldx,
+                         void* stream, int variant) {
+  int rc = validate_apply(sk, Y, ldy, sk ? sk->k : 0, n, BPS_F32, X, ldx, sk ? sk->d : 0, n, variant);
+  if (rc || n == 0) return rc;
+  if ((rc = check_device())) return rc;
+  const bool tc = bps::adjoint_tc_supported(sk->p, n);
+  if (variant == BPS_VARIANT_TC && !tc) return fail(BPS_ERR_UNSUPPORTED, "adjoint tc: shape not covered");
+  if (variant != BPS_VARIANT_SPARSE && tc) return bps::launch_adjoint_tc(sk->p, Y, ldy, n, X, ldx, (cudaStream_t)stream);
+  return launch_adjoint(sk->p, Y, ldy, n, X, ldx, (cudaStream_t)stream);
+}
+
+int bps_apply_adjoint(const bps_sketch* sk, const float* Y, int64_t ldy, int64_t n, float* X, int64_t ldx,
+                      void* stream) {
+  return bps_apply_adjoint_ex(sk, Y, ldy, n, X, ldx, stream, BPS_VARIANT_AUTO);
+}
+
 int bps_apply_orbit_range(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end, const void* A_local, int64_t lda,
                           int64_t n, bps_dtype dtype, float* Y_local, int64_t ldy, void* stream, int variant) {
   if (!sk) return fail(BPS_ERR_INVALID_ARG, "sketch handle is NULL");

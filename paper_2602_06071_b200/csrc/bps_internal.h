@@ -44,4 +44,12 @@ size_t tc_workspace_bytes(const SketchParams& p, int64_t n, bps_dtype dt, bool t
 int launch_tc(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt, float* Y, int64_t ldy,
               bool transposed, const Placement& pl, void* ws, size_t ws_bytes, cudaStream_t st);
 
+// Adjoint X = Sᵀ·Y (bps_adjoint.cu).
+int launch_adjoint(const SketchParams& p, const float* Y, int64_t ldy, int64_t n, float* X, int64_t ldx,
+                   cudaStream_t st);
+// tcgen05 adjoint (bps_adjoint_tc.cu).
+int adjoint_tc_supported(const SketchParams& p, int64_t n);
+int launch_adjoint_tc(const SketchParams& p, const float* Y, int64_t ldy, int64_t n, float* X, int64_t ldx,
+                      cudaStream_t st);
+
 }  // namespace bps

@@ -116,6 +116,23 @@ class Sketch:
                                VARIANTS[variant]))
         return out
 
+    def apply_adjoint(self, Y, out=None, variant: str = "auto"):
+        """X = Sᵀ·Y. Y: cuda k×n float32 (row-major) -> d×n float32 (bps_apply_adjoint)."""
+        import torch
+
+        _check_matrix(Y, "Y")
+        if Y.shape[0] != self.k or Y.dtype != torch.float32:
+            raise ValueError(f"Y must be float32 with k={self.k} rows")
+        n = Y.shape[1]
+        if out is None:
+            out = torch.empty((self.d, n), dtype=torch.float32, device=Y.device)
+        _check_matrix(out, "out")
+        if out.dtype != torch.float32 or tuple(out.shape) != (self.d, n):
+            raise ValueError("out must be float32 d×n")
+        check(lib.bps_apply_adjoint_ex(self._h, Y.data_ptr(), Y.stride(0), n, out.data_ptr(), out.stride(0),
+                                       _stream_ptr(Y.device), VARIANTS[variant]))
+        return out
+
     def apply_t(self, X, out=None, variant: str = "auto", use_workspace: bool = True):
         """Transposed layout: X cuda n×d -> (S·Xᵀ)ᵀ, n×k float32."""
         import torch

@@ -59,6 +59,11 @@ def test_null_handle_and_apply_validation():
     assert lib.bps_apply(h, 0x1000, 16, 16, 0, 0x1000, 16, None) == -1
     # bad orbit range
     assert lib.bps_apply_orbit_range(h, 8, 9, 0x1000, 16, 16, 0, 0x100000000, 16, None, 0) == -1
+    # adjoint: NULL / misaligned / overlapping arguments rejected before device work
+    assert lib.bps_apply_adjoint(h, None, 16, 0, None, 16, None) == 0
+    assert lib.bps_apply_adjoint(h, None, 16, 16, None, 16, None) == -1
+    assert lib.bps_apply_adjoint(h, 0x1004, 16, 16, 0x100000000, 16, None) == -2
+    assert lib.bps_apply_adjoint(h, 0x1000, 16, 16, 0x1000, 16, None) == -1
     lib.bps_free_sketch(h)
     lib.bps_free_sketch(None)
 
