@@ -21,6 +21,7 @@ Pins (what checks the oracle against something other than itself) live in
 pin say "parity unpinned" in their docstring (none at present).
 """
 
+from . import blockrow  # noqa: F401  (FlashBlockRow, P:1424-1466)
 from .blockperm import (  # noqa: F401
     MASK64,
     TAG_A,
