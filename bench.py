@@ -44,6 +44,8 @@ def parse():
                          "block: strong scaling of one d×n problem sharded along the wiring orbit + all-gather")
     ap.add_argument("--op", default="apply", choices=["apply", "adjoint"],
                     help="adjoint: X = Sᵀ·Y (fp32 k×n -> d×n) on the same sketch; secondary line, no e2e/cpu legs")
+    ap.add_argument("--sketch", default="blockperm", choices=["blockperm", "blockrow"],
+                    help="blockrow: the FlashBlockRow sampling sketch (P:1424-1466); secondary line")
     ap.add_argument("--no-workspace", action="store_true", help="block-aligned ranges (no balanced workspace)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -193,7 +195,9 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     n = cfg.n
     tdt = torch.float32 if cfg.dtype == "f32" else torch.bfloat16
-    sk = Sketch(**cfg.sketch_args())
+    sk = Sketch(**cfg.sketch_args(), kind=args.sketch)
+    if args.sketch == "blockrow":  # secondary line: the e2e/cpu legs are defined for the main sketch
+        args.no_cpu_baseline = args.no_e2e = True
     stream = torch.cuda.current_stream(dev)
     if args.shard == "block" and world > 1:
         from paper_2602_06071_b200 import dist as D
@@ -252,6 +256,8 @@ def main():
     bytes_rank = cfg.roofline_bytes(n) if not block else cfg.roofline_bytes(n) // world
     if args.op == "adjoint":  # read Y (k×n fp32) once, write X (d×n fp32) once
         bytes_rank = (cfg.k + cfg.d) * n * 4
+    if args.sketch == "blockrow":  # gather: κs sampled input rows per output row, one fp32 write
+        bytes_rank = cfg.k * n * (cfg.kappa * cfg.s * cfg.elem + 4)
     value = world * bytes_rank / (ms / 1e3) / 1e9
     peak, peak_src = measured_peaks()
     achieved = bytes_rank / (statistics.mean(per) / 1e3) / 1e9
@@ -303,13 +309,14 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC if args.op == "apply" else "adjoint_throughput_gbs", "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": ("blockrow_gather_gbs" if args.sketch == "blockrow" else METRIC) if args.op == "apply"
+            else "adjoint_throughput_gbs", "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if block else "weak",
             "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" or args.op == "adjoint" else "bf16-in/f32-acc",
             "data": f"synthetic {args.kind} (torch Philox on device), seed {1000}+rank",
             "config": {"workload": cfg.name, "d": cfg.d, "k": cfg.k, "kappa": cfg.kappa, "s": cfg.s,
-                       "n_per_gpu": n, "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c, "variant": args.variant, "op": args.op,
+                       "n_per_gpu": n, "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c, "variant": args.variant, "op": args.op, "sketch": args.sketch,
                        "parallelism": (f"orbit-block-shard x{world} + NCCL all_gather" if block
                                        else f"column-shard x{world} (no collective)"),
                        "l2": "inputs larger than L2 (no flush needed)" if bytes_rank > (256 << 20) else "input fits L2"},
@@ -318,7 +325,7 @@ def main():
             "frac_of_8tbs": value / world / 8000.0,
             "ms_min": min(per), "ms_median": statistics.median(per),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic(cfg.name, args.variant) if args.op == "apply" else None, "peak_source": peak_src,
+                         "traffic": ncu_traffic(cfg.name, args.variant) if (args.op == "apply" and args.sketch == "blockperm") else None, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": bytes_rank},
             "gpu_launches": launches,
             "clocks": clk,

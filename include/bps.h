@@ -150,6 +150,29 @@ int bps_apply_adjoint_ex(const bps_sketch* sk, const float* Y, int64_t ldy, int6
                          int64_t ldx, void* stream, int variant);
 
 /*
+ * FlashBlockRow (Alg. alg:blockrowsketch P:1447-1464) — the
+ * paper's "fast but fragile" block-row sampling sketch S' (a different matrix from BlockPerm-SJLT):
+ *   output block g gathers from κ distinct input blocks N_row(g) ⊂ [M] (R14); output row r adds
+ *   s uniformly sampled rows i ∈ [B_c] (with replacement) of each, with Rademacher signs (R15):
+ *   Y[g·B_r + r, :] = (κs)^{-1/2}·(d/k)^{1/2}·Σ_{h∈N_row(g)} Σ_t σ_t A[h·B_c + i_t, :]   (R16, R17)
+ * bps_make_blockrow: 1 ≤ κ ≤ min(M, 256), 1 ≤ s ≤ 256, M, B_r, B_c < 2^24 (no B_r % s rule);
+ *   BPS_ERR_INVALID_ARG otherwise.  The handle works with bps_apply / bps_apply_t / _ex / _ws
+ *   (variant AUTO or SPARSE = the gather kernel; TC -> BPS_ERR_UNSUPPORTED; workspace size 0);
+ *   bps_apply_orbit_range, bps_apply_adjoint, bps_orbit and bps_pattern_host return
+ *   BPS_ERR_UNSUPPORTED / BPS_ERR_INVALID_ARG for it.  bps_sketch_info reports a = b = 0 and
+ *   the block-row scale.  Transposed apply needs κ·s ≤ 4096.
+ * bps_blockrow_neighbors: host, N_row(g) in draw order (ℓ = 1..κ) into nb[κ].
+ * bps_blockrow_draw_host: host, (i, sign) of sample t of row r for the ℓ-th neighbour (ell 1-based).
+ * bps_sketch_kind: 0 = BlockPerm-SJLT, 1 = FlashBlockRow, negative on a NULL handle.
+ */
+int bps_make_blockrow(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t s, uint64_t seed,
+                      bps_sketch** out);
+int bps_blockrow_neighbors(const bps_sketch* sk, int64_t g, int32_t* nb);
+int bps_blockrow_draw_host(const bps_sketch* sk, int64_t g, int32_t ell, int64_t r, int32_t t,
+                           int32_t* i, int32_t* sign);
+int bps_sketch_kind(const bps_sketch* sk);
+
+/*
  * bps_orbit — the wiring orbit g_pos = f^pos(0), pos = 0..M-1 (host).
  *   With this ordering N(g_i) = (g_{i+1}, ..., g_{i+κ}) (indices mod M), which is what
  *   makes block sharding contiguous.  g_of_pos: host array of length M.

@@ -64,6 +64,14 @@ def _load() -> ctypes.CDLL:
     L.bps_apply_adjoint.restype = ctypes.c_int
     L.bps_apply_adjoint_ex.argtypes = [vp, vp, i64, i64, vp, i64, vp, ctypes.c_int]
     L.bps_apply_adjoint_ex.restype = ctypes.c_int
+    L.bps_make_blockrow.argtypes = [i64, i64, i64, i32, i32, u64, ctypes.POINTER(vp)]
+    L.bps_make_blockrow.restype = ctypes.c_int
+    L.bps_blockrow_neighbors.argtypes = [vp, i64, ctypes.POINTER(i32)]
+    L.bps_blockrow_neighbors.restype = ctypes.c_int
+    L.bps_blockrow_draw_host.argtypes = [vp, i64, i32, i64, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    L.bps_blockrow_draw_host.restype = ctypes.c_int
+    L.bps_sketch_kind.argtypes = [vp]
+    L.bps_sketch_kind.restype = ctypes.c_int
     L.bps_orbit.argtypes = [vp, ctypes.POINTER(i32)]
     L.bps_orbit.restype = ctypes.c_int
     L.bps_apply_orbit_range.argtypes = [vp, i64, i64, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_int]

@@ -117,6 +117,11 @@ static int dispatch(const bps_sketch* sk, const void* in, int64_t ldin, int64_t 
   int rc = check_device();
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  if (sk->kind == 1) {  // FlashBlockRow: one gather kernel (no tcgen05 variant, no ranges, no workspace)
+    if (variant == BPS_VARIANT_TC) return fail(BPS_ERR_UNSUPPORTED, "blockrow sketch: only the gather kernel");
+    if (pl.range_mode) return fail(BPS_ERR_UNSUPPORTED, "blockrow sketch: no orbit ranges");
+    return launch_blockrow(sk->br, in, ldin, n, dt, out, ldout, transposed, st);
+  }
   const bool tc_ok = tc_supported(sk->p, n, dt, transposed, pl) == BPS_OK;
   if (variant == BPS_VARIANT_TC && !tc_ok) return BPS_ERR_UNSUPPORTED;  // message set by tc_supported
   if (tc_ok && variant != BPS_VARIANT_SPARSE)
@@ -150,6 +155,8 @@ int bps_make_sketch(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t 
   if (M > (int64_t(1) << 62) / B_c || M > (int64_t(1) << 62) / B_r) return fail(BPS_ERR_OVERFLOW, "M*B_c or M*B_r overflows");
   bps_sketch* sk = new (std::nothrow) bps_sketch;
   if (!sk) return fail(BPS_ERR_INVALID_ARG, "out of host memory");
+  sk->kind = 0;
+  sk->br = BlockRowParams{};
   sk->M = M;
   sk->B_r = B_r;
   sk->B_c = B_c;
@@ -173,6 +180,68 @@ int bps_make_sketch(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t 
   return BPS_OK;
 }
 
+int bps_make_blockrow(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t s, uint64_t seed,
+                      bps_sketch** out) {
+  if (!out) return fail(BPS_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (M < 1 || B_r < 1 || B_c < 1) return fail(BPS_ERR_INVALID_ARG, "M, B_r, B_c must be >= 1");
+  if (M >= (int64_t(1) << 24) || B_r >= (int64_t(1) << 24) || B_c >= (int64_t(1) << 24))
+    return fail(BPS_ERR_INVALID_ARG, "M, B_r, B_c must be < 2^24 (counter fields, R15)");
+  if (kappa < 1 || kappa > M || kappa > 256) return fail(BPS_ERR_INVALID_ARG, "need 1 <= kappa <= min(M, 256) (R14)");
+  if (s < 1 || s > 256) return fail(BPS_ERR_INVALID_ARG, "need 1 <= s <= 256 (R15)");
+  bps_sketch* sk = new (std::nothrow) bps_sketch;
+  if (!sk) return fail(BPS_ERR_INVALID_ARG, "out of host memory");
+  sk->kind = 1;
+  sk->p = SketchParams{};
+  sk->M = M;
+  sk->B_r = B_r;
+  sk->B_c = B_c;
+  sk->d = M * B_c;
+  sk->k = M * B_r;
+  sk->kappa = kappa;
+  sk->s = s;
+  sk->seed = seed;
+  BlockRowParams& p = sk->br;
+  p.M = (uint32_t)M;
+  p.B_r = (uint32_t)B_r;
+  p.B_c = (uint32_t)B_c;
+  p.kappa = (uint32_t)kappa;
+  p.s = (uint32_t)s;
+  p.Kb = mix64(seed ^ kTagRowBlk);
+  p.Ki = mix64(seed ^ kTagRowIdx);
+  p.scale = (float)(std::sqrt((double)B_c / (double)B_r) / std::sqrt((double)kappa * (double)s));
+  *out = sk;
+  return BPS_OK;
+}
+
+int bps_blockrow_neighbors(const bps_sketch* sk, int64_t g, int32_t* nb) {
+  if (!sk || !nb) return fail(BPS_ERR_INVALID_ARG, "NULL argument");
+  if (sk->kind != 1) return fail(BPS_ERR_INVALID_ARG, "not a blockrow sketch");
+  if (g < 0 || g >= sk->M) return fail(BPS_ERR_INVALID_ARG, "g out of range");
+  int cnt = 0;
+  for (uint32_t t = 0; cnt < sk->kappa; ++t) {
+    const uint32_t h = br_block_draw(sk->br, (uint32_t)g, t);
+    bool dup = false;
+    for (int j = 0; j < cnt; ++j) dup |= (uint32_t)nb[j] == h;
+    if (!dup) nb[cnt++] = (int32_t)h;
+  }
+  return BPS_OK;
+}
+
+int bps_blockrow_draw_host(const bps_sketch* sk, int64_t g, int32_t ell, int64_t r, int32_t t, int32_t* i,
+                           int32_t* sign) {
+  if (!sk || !i || !sign) return fail(BPS_ERR_INVALID_ARG, "NULL argument");
+  if (sk->kind != 1) return fail(BPS_ERR_INVALID_ARG, "not a blockrow sketch");
+  if (g < 0 || g >= sk->M || ell < 1 || ell > sk->kappa || r < 0 || r >= sk->B_r || t < 0 || t >= sk->s)
+    return fail(BPS_ERR_INVALID_ARG, "index out of range");
+  const BrDraw dr = br_index_draw(sk->br, (uint32_t)g, (uint32_t)ell, (uint32_t)r, (uint32_t)t);
+  *i = (int32_t)dr.i;
+  *sign = dr.neg ? -1 : 1;
+  return BPS_OK;
+}
+
+int bps_sketch_kind(const bps_sketch* sk) { return sk ? sk->kind : fail(BPS_ERR_INVALID_ARG, "sketch handle is NULL"); }
+
 void bps_free_sketch(bps_sketch* sk) { delete sk; }
 
 int bps_sketch_info(const bps_sketch* sk, int64_t* d, int64_t* k, uint32_t* a, uint32_t* b, float* scale) {
@@ -181,12 +250,13 @@ int bps_sketch_info(const bps_sketch* sk, int64_t* d, int64_t* k, uint32_t* a, u
   if (k) *k = sk->k;
   if (a) *a = sk->p.a;
   if (b) *b = sk->p.b;
-  if (scale) *scale = sk->p.scale;
+  if (scale) *scale = sk->kind == 1 ? sk->br.scale : sk->p.scale;
   return BPS_OK;
 }
 
 int bps_orbit(const bps_sketch* sk, int32_t* g_of_pos) {
   if (!sk || !g_of_pos) return fail(BPS_ERR_INVALID_ARG, "NULL argument");
+  if (sk->kind != 0) return fail(BPS_ERR_UNSUPPORTED, "orbit: BlockPerm-SJLT sketches only");
   uint32_t x = 0;
   for (int64_t i = 0; i < sk->M; ++i) {
     g_of_pos[i] = (int32_t)x;
@@ -197,6 +267,7 @@ int bps_orbit(const bps_sketch* sk, int32_t* g_of_pos) {
 
 int bps_pattern_host(const bps_sketch* sk, int64_t g, int32_t ell, int64_t u, int32_t j, int32_t* row, int32_t* sign) {
   if (!sk || !row || !sign) return fail(BPS_ERR_INVALID_ARG, "NULL argument");
+  if (sk->kind != 0) return fail(BPS_ERR_INVALID_ARG, "pattern: BlockPerm-SJLT sketches only");
   if (g < 0 || g >= sk->M || ell < 1 || ell > sk->kappa || u < 0 || u >= sk->B_c || j < 0 || j >= sk->s)
     return fail(BPS_ERR_INVALID_ARG, "index out of range");
   Draw dr = pattern(sk->p, (uint32_t)g, (uint32_t)ell, (uint32_t)u, (uint32_t)j);
@@ -235,7 +306,7 @@ int bps_workspace_size(const bps_sketch* sk, int64_t n, bps_dtype dtype, int tra
   if (!sk || !bytes) return fail(BPS_ERR_INVALID_ARG, "NULL argument");
   if (n < 0) return fail(BPS_ERR_INVALID_ARG, "negative n");
   Placement pl{0, 0, sk->M};
-  *bytes = tc_workspace_bytes(sk->p, n, dtype, transposed != 0, pl);
+  *bytes = sk->kind ? 0 : tc_workspace_bytes(sk->p, n, dtype, transposed != 0, pl);
   return BPS_OK;
 }
 
@@ -263,6 +334,7 @@ int bps_apply_adjoint_ex(const bps_sketch* sk, const float* Y, int64_t ldy, int6
                          void* stream, int variant) {
   int rc = validate_apply(sk, Y, ldy, sk ? sk->k : 0, n, BPS_F32, X, ldx, sk ? sk->d : 0, n, variant);
   if (rc || n == 0) return rc;
+  if (sk->kind != 0) return fail(BPS_ERR_UNSUPPORTED, "adjoint: BlockPerm-SJLT sketches only");
   if ((rc = check_device())) return rc;
   const bool tc = bps::adjoint_tc_supported(sk->p, n);
   if (variant == BPS_VARIANT_TC && !tc) return fail(BPS_ERR_UNSUPPORTED, "adjoint tc: shape not covered");

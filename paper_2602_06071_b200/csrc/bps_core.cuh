@@ -14,6 +14,8 @@ namespace bps {
 constexpr uint64_t kTagA = 0xA11CE5EEDA11CE5EULL;
 constexpr uint64_t kTagB = 0xB0B5EEDB0B5EEDB0ULL;
 constexpr uint64_t kTagPhi = 0x5048495F5048495FULL;
+constexpr uint64_t kTagRowBlk = 0x524F57424C4F434BULL;  // "ROWBLOCK" (R14)
+constexpr uint64_t kTagRowIdx = 0x524F57494E444558ULL;  // "ROWINDEX" (R15)
 
 // MurmurHash3 fmix64 (R2; "fast mixing hash").
 BPS_HD uint64_t mix64(uint64_t z) {
@@ -91,6 +93,31 @@ BPS_HD Draw draw_from_hash(const SketchParams& p, uint64_t z, uint32_t j) {
 
 BPS_HD Draw pattern(const SketchParams& p, uint32_t g, uint32_t ell, uint32_t u, uint32_t j) {
   return draw_from_hash(p, pattern_hash(p, g, ell, u, j), j);
+}
+
+// ---------------------------------------------------------------- FlashBlockRow (R14-R16)
+struct BlockRowParams {
+  uint32_t M, B_r, B_c, kappa, s;
+  uint64_t Kb, Ki;  // fmix64(seed ^ "ROWBLOCK"), fmix64(seed ^ "ROWINDEX")
+  float scale;      // (κs)^{-1/2}·(d/k)^{1/2}
+};
+
+// attempt t of the rejection draw of N_row(g): a uniform block in [M) (R14)
+BPS_HD uint32_t br_block_draw(const BlockRowParams& p, uint32_t g, uint32_t t) {
+  const uint64_t z = mix64((((uint64_t)g << 32) | (uint64_t)t) ^ p.Kb);
+  return (uint32_t)(((z >> 32) * (uint64_t)p.M) >> 32);
+}
+
+struct BrDraw {
+  uint32_t i;    // row inside the input block, uniform in [B_c)
+  uint32_t neg;  // 1 => sign -1
+};
+
+// sample t of output row r for the ℓ-th neighbour (ℓ 1-based) of output block g (R15)
+BPS_HD BrDraw br_index_draw(const BlockRowParams& p, uint32_t g, uint32_t ell, uint32_t r, uint32_t t) {
+  const uint64_t ctr = ((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | ((uint64_t)r << 8) | (uint64_t)t;
+  const uint64_t z = mix64(ctr ^ p.Ki);
+  return BrDraw{(uint32_t)(((z >> 32) * (uint64_t)p.B_c) >> 32), (uint32_t)(z & 1)};
 }
 
 }  // namespace bps

@@ -10,7 +10,9 @@
 #include "bps_core.cuh"
 
 struct bps_sketch {
+  int kind;  // 0 = BlockPerm-SJLT, 1 = FlashBlockRow
   bps::SketchParams p;
+  bps::BlockRowParams br;
   int64_t M, B_r, B_c, d, k;
   int32_t kappa, s;
   uint64_t seed;
@@ -47,6 +49,9 @@ int launch_tc(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_
 // Adjoint X = Sᵀ·Y (bps_adjoint.cu).
 int launch_adjoint(const SketchParams& p, const float* Y, int64_t ldy, int64_t n, float* X, int64_t ldx,
                    cudaStream_t st);
+// FlashBlockRow gather kernels (bps_blockrow.cu).
+int launch_blockrow(const BlockRowParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt, float* Y,
+                    int64_t ldy, bool transposed, cudaStream_t st);
 // tcgen05 adjoint (bps_adjoint_tc.cu).
 int adjoint_tc_supported(const SketchParams& p, int64_t n);
 int launch_adjoint_tc(const SketchParams& p, const float* Y, int64_t ldy, int64_t n, float* X, int64_t ldx,

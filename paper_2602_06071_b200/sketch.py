@@ -36,11 +36,14 @@ def _check_matrix(t, name):
 
 
 class Sketch:
-    """BlockPerm-SJLT S (k×d, k = M·B_r, d = M·B_c) regenerated on the fly (bps_make_sketch)."""
+    """BlockPerm-SJLT S (k×d, k = M·B_r, d = M·B_c) regenerated on the fly (bps_make_sketch);
+    kind="blockrow": the FlashBlockRow sampling sketch of P:1424-1466 (bps_make_blockrow)."""
 
-    def __init__(self, M: int, B_r: int, B_c: int, kappa: int, s: int, seed: int = 0):
+    def __init__(self, M: int, B_r: int, B_c: int, kappa: int, s: int, seed: int = 0, kind: str = "blockperm"):
         h = ctypes.c_void_p()
-        check(lib.bps_make_sketch(M, B_r, B_c, kappa, s, ctypes.c_uint64(seed & (2**64 - 1)), ctypes.byref(h)))
+        make = {"blockperm": lib.bps_make_sketch, "blockrow": lib.bps_make_blockrow}[kind]
+        check(make(M, B_r, B_c, kappa, s, ctypes.c_uint64(seed & (2**64 - 1)), ctypes.byref(h)))
+        self.kind = kind
         self._h = h
         self.M, self.B_r, self.B_c, self.kappa, self.s, self.seed = M, B_r, B_c, kappa, s, seed & (2**64 - 1)
         d, k = ctypes.c_int64(), ctypes.c_int64()
@@ -62,6 +65,17 @@ class Sketch:
     def info(self) -> dict:
         return dict(M=self.M, B_r=self.B_r, B_c=self.B_c, kappa=self.kappa, s=self.s, seed=self.seed,
                     d=self.d, k=self.k, a=self.a, b=self.b, scale=self.scale)
+
+    def neighbors_row(self, g: int) -> list[int]:
+        """FlashBlockRow N_row(g) in draw order (R14)."""
+        arr = (ctypes.c_int32 * self.kappa)()
+        check(lib.bps_blockrow_neighbors(self._h, g, arr))
+        return list(arr)
+
+    def blockrow_draw(self, g: int, ell: int, r: int, t: int) -> tuple[int, int]:
+        i, sg = ctypes.c_int32(), ctypes.c_int32()
+        check(lib.bps_blockrow_draw_host(self._h, g, ell, r, t, ctypes.byref(i), ctypes.byref(sg)))
+        return i.value, sg.value
 
     def orbit(self) -> list[int]:
         arr = (ctypes.c_int32 * self.M)()

@@ -107,3 +107,41 @@ def test_apply_without_gpu_fails_loudly():
     A = torch.zeros((C.TINY.d, 16))
     with pytest.raises(ValueError):
         sk.apply(A)  # CPU tensor: no CPU path
+
+
+def test_blockrow_host_derivation_matches_oracle():
+    """FlashBlockRow N_row(g) and (i, sign) draws of libbps equal the oracle's bit-exactly (R14-R16)."""
+    import numpy as np
+
+    from oracle import blockrow as BR
+
+    for layout, seed in [((8, 4, 16, 2, 2), 3), ((128, 32, 8192, 4, 4), 1234), ((7, 5, 9, 7, 3), 2**63 + 5)]:
+        sk = Sketch(*layout, seed=seed, kind="blockrow")
+        br = BR.make_blockrow(*layout, seed=seed)
+        assert lib.bps_sketch_kind(sk.handle) == 1
+        assert np.float32(br.scale) == np.float32(sk.scale)
+        assert (sk.d, sk.k) == (br.d, br.k)
+        rng = np.random.default_rng(0)
+        for g in rng.choice(br.M, min(br.M, 6), replace=False):
+            g = int(g)
+            assert sk.neighbors_row(g) == BR.neighbors_row(br, g)
+            for _ in range(10):
+                ell = int(rng.integers(1, br.kappa + 1))
+                r, t = int(rng.integers(br.B_r)), int(rng.integers(br.s))
+                assert sk.blockrow_draw(g, ell, r, t) == BR.draw_index(br, g, ell, r, t)
+
+
+def test_blockrow_validation_and_unsupported_calls():
+    for args in [(4, 2, 2, 5, 1), (4, 2, 2, 0, 1), (4, 2, 2, 2, 0), (4, 2, 2, 2, 300), (1 << 24, 1, 1, 1, 1)]:
+        with pytest.raises(BpsError) as e:
+            Sketch(*args, seed=0, kind="blockrow")
+        assert e.value.code == -1
+    sk = Sketch(8, 4, 16, 2, 3, seed=1, kind="blockrow")  # B_r % s != 0 is fine here
+    with pytest.raises(BpsError):
+        sk.orbit()
+    with pytest.raises(BpsError):
+        sk.pattern(0, 1, 0, 0)
+    bp = Sketch(8, 32, 128, 2, 2, seed=1)
+    assert lib.bps_sketch_kind(bp.handle) == 0
+    with pytest.raises(BpsError):
+        bp.neighbors_row(0)
