@@ -183,6 +183,7 @@ class Sketch:
     a: int
     b: int
     K: int  # mix64(seed ^ TAG_PHI), R2
+    mode: str = "rowpart"  # intra-block rows: "rowpart" (R1, R3) or "affine" (AffineUnique, R18)
 
     @property
     def d(self) -> int:
@@ -203,20 +204,26 @@ class Sketch:
         return 1.0 / math.sqrt(self.kappa * self.s)
 
 
-def make_sketch(M: int, B_r: int, B_c: int, kappa: int, s: int, seed: int) -> Sketch:
+def make_sketch(M: int, B_r: int, B_c: int, kappa: int, s: int, seed: int, mode: str = "rowpart") -> Sketch:
     """Validate (1≤κ≤M, 1≤s≤B_r, B_r mod s = 0; counter widths R2) and
-    derive (a, b, K)."""
+    derive (a, b, K).  mode="affine" (R18): B_r a power of two ≤ 2^16, s ≤ min(B_r, 32), no
+    divisibility rule."""
     if M < 1 or B_r < 1 or B_c < 1:
         raise ValueError("M, B_r, B_c must be >= 1")
     if not (1 <= kappa <= M):
         raise ValueError("need 1 <= kappa <= M (P:1531)")
-    if not (1 <= s <= B_r) or B_r % s != 0:
+    if mode == "affine":
+        if B_r & (B_r - 1) or B_r > 1 << 16 or not (1 <= s <= min(B_r, 32)):
+            raise ValueError("affine mode: B_r a power of two <= 2^16 and 1 <= s <= min(B_r, 32) (R18)")
+    elif mode != "rowpart":
+        raise ValueError("mode must be 'rowpart' or 'affine'")
+    elif not (1 <= s <= B_r) or B_r % s != 0:
         raise ValueError("need 1 <= s <= B_r and B_r % s == 0 (row-partitioned, R1)")
     if M >= 1 << 24 or B_c >= 1 << 24 or kappa > 256 or s > 256:
         raise ValueError("counter field widths exceeded (R2)")
     seed &= MASK64
     a, b = select_affine(seed, M)
-    return Sketch(M, B_r, B_c, kappa, s, seed, a, b, mix64(seed ^ TAG_PHI))
+    return Sketch(M, B_r, B_c, kappa, s, seed, a, b, mix64(seed ^ TAG_PHI), mode)
 
 
 def pattern(sk: Sketch, g: int, ell: int, u: int, j: int) -> tuple[int, int]:
@@ -227,10 +234,31 @@ def pattern(sk: Sketch, g: int, ell: int, u: int, j: int) -> tuple[int, int]:
     ctr = g<<40 | (ℓ-1)<<32 | u<<8 | j ;  z = mix64(ctr ^ K)
     row = j·C + ((z>>32)·C >> 32) ;  sign = -1 if z&1 else +1
     """
+    if sk.mode == "affine":
+        return pattern_affine(sk, g, ell, u, j)
     ctr = (g << 40) | ((ell - 1) << 32) | (u << 8) | j
     z = mix64(ctr ^ sk.K)
     off = ((z >> 32) * sk.C) >> 32
     return j * sk.C + off, (-1 if (z & 1) else 1)
+
+
+def affine_params(sk: Sketch, g: int, ell: int, u: int) -> tuple[int, int, int]:
+    """R18 (AffineUnique: "s unique row indices using an affine permutation map ...
+    with scale and shift parameters generated from the hash"): one hash per column u of
+    Φ_{g,π_ℓ(g)}:  z = mix64((g<<40 | (ℓ-1)<<32 | u<<8) ^ K);
+    scale α = (((z>>32) & 0xFFFF)·B_r >> 16) | 1  (odd: a unit mod the power of two B_r),
+    shift β = ((z>>48)·B_r) >> 16.  Returns (α, β, z)."""
+    z = mix64(((g << 40) | ((ell - 1) << 32) | (u << 8)) ^ sk.K)
+    alpha = ((((z >> 32) & 0xFFFF) * sk.B_r) >> 16) | 1
+    beta = ((z >> 48) * sk.B_r) >> 16
+    return alpha, beta, z
+
+
+def pattern_affine(sk: Sketch, g: int, ell: int, u: int, j: int) -> tuple[int, int]:
+    """R18: row_j = (α·j + β) mod B_r — the first s images of the permutation x ↦ αx+β of
+    [B_r], hence s distinct rows; sign_j = −1 iff bit j of z is set (j < 32)."""
+    alpha, beta, z = affine_params(sk, g, ell, u)
+    return (alpha * j + beta) % sk.B_r, (-1 if (z >> j) & 1 else 1)
 
 
 def _block_entries(sk: Sketch, g: int):
@@ -240,6 +268,18 @@ def _block_entries(sk: Sketch, g: int):
     u = np.arange(sk.B_c, dtype=np.uint64)
     rows, cols, vals = [], [], []
     for ell, h in enumerate(nbr, start=1):
+        if sk.mode == "affine":
+            ctr = (np.uint64(g) << np.uint64(40)) | (np.uint64(ell - 1) << np.uint64(32)) | (u << np.uint64(8))
+            z = mix64(ctr ^ np.uint64(sk.K))
+            alpha = ((((z >> np.uint64(32)) & np.uint64(0xFFFF)) * np.uint64(sk.B_r)) >> np.uint64(16)) | np.uint64(1)
+            beta = ((z >> np.uint64(48)) * np.uint64(sk.B_r)) >> np.uint64(16)
+            for j in range(sk.s):
+                row = (alpha * np.uint64(j) + beta) % np.uint64(sk.B_r)
+                sign = np.where(((z >> np.uint64(j)) & np.uint64(1)) == 1, -1.0, 1.0)
+                rows.append(g * sk.B_r + row.astype(np.int64))
+                cols.append(h * sk.B_c + u.astype(np.int64))
+                vals.append(sign * sk.scale)
+            continue
         for j in range(sk.s):
             ctr = (np.uint64(g) << np.uint64(40)) | (np.uint64(ell - 1) << np.uint64(32)) | (u << np.uint64(8)) | np.uint64(j)
             z = mix64(ctr ^ np.uint64(sk.K))
