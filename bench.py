@@ -46,6 +46,8 @@ def parse():
                     help="adjoint: X = Sᵀ·Y (fp32 k×n -> d×n) on the same sketch; secondary line, no e2e/cpu legs")
     ap.add_argument("--sketch", default="blockperm", choices=["blockperm", "blockrow"],
                     help="blockrow: the FlashBlockRow sampling sketch (P:1424-1466); secondary line")
+    ap.add_argument("--mode", default="rowpart", choices=["rowpart", "affine"],
+                    help="intra-block pattern of BlockPerm-SJLT: row-partitioned (R1) or AffineUnique (R18)")
     ap.add_argument("--no-workspace", action="store_true", help="block-aligned ranges (no balanced workspace)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -195,7 +197,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     n = cfg.n
     tdt = torch.float32 if cfg.dtype == "f32" else torch.bfloat16
-    sk = Sketch(**cfg.sketch_args(), kind=args.sketch)
+    sk = Sketch(**cfg.sketch_args(), kind=args.sketch, **({"mode": args.mode} if args.sketch == "blockperm" else {}))
     if args.sketch == "blockrow":  # secondary line: the e2e/cpu legs are defined for the main sketch
         args.no_cpu_baseline = args.no_e2e = True
     stream = torch.cuda.current_stream(dev)
@@ -316,7 +318,7 @@ def main():
             "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" or args.op == "adjoint" else "bf16-in/f32-acc",
             "data": f"synthetic {args.kind} (torch Philox on device), seed {1000}+rank",
             "config": {"workload": cfg.name, "d": cfg.d, "k": cfg.k, "kappa": cfg.kappa, "s": cfg.s,
-                       "n_per_gpu": n, "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c, "variant": args.variant, "op": args.op, "sketch": args.sketch,
+                       "n_per_gpu": n, "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c, "variant": args.variant, "op": args.op, "sketch": args.sketch, "mode": args.mode,
                        "parallelism": (f"orbit-block-shard x{world} + NCCL all_gather" if block
                                        else f"column-shard x{world} (no collective)"),
                        "l2": "inputs larger than L2 (no flush needed)" if bytes_rank > (256 << 20) else "input fits L2"},

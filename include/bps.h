@@ -53,6 +53,12 @@ typedef enum {
   BPS_ERR_OVERFLOW = -6     /* a size product does not fit the supported integer range */
 } bps_status;
 
+/* Intra-block pattern of Φ_{g,h} (bps_make_sketch_ex). */
+typedef enum {
+  BPS_MODE_ROWPART = 0, /* row-partitioned SJLT: chunk j = rows [jC,(j+1)C), C = B_r/s (R1, R3); default */
+  BPS_MODE_AFFINE = 1   /* AffineUnique (R18): rows (α·j + β) mod B_r from one hash per column */
+} bps_mode;
+
 /* Kernel variant selector for bps_apply_ex / bps_apply_t_ex. */
 typedef enum {
   BPS_VARIANT_AUTO = 0,   /* tcgen05 path when supported for the shape, else the sparse path */
@@ -148,6 +154,19 @@ int bps_apply_adjoint(const bps_sketch* sk, const float* Y, int64_t ldy, int64_t
                       int64_t ldx, void* stream);
 int bps_apply_adjoint_ex(const bps_sketch* sk, const float* Y, int64_t ldy, int64_t n, float* X,
                          int64_t ldx, void* stream, int variant);
+
+/*
+ * bps_make_sketch_ex — bps_make_sketch with the intra-block pattern mode (bps_mode).
+ *   BPS_MODE_AFFINE (R18): same wiring, scale and counter
+ *   fields; column u of Φ_{g,f^ℓ(g)} takes z = fmix64((g≪40 | (ℓ−1)≪32 | u≪8) ⊕ K),
+ *   α = (((z≫32) & 0xFFFF)·B_r ≫ 16) | 1, β = ((z≫48)·B_r) ≫ 16, rows (α·j + β) mod B_r and
+ *   signs = bit j of z, j < s.  Requires B_r a power of two ≤ 2^16 and 1 ≤ s ≤ min(B_r, 32)
+ *   (no B_r % s rule), else BPS_ERR_INVALID_ARG.  Every entry point accepts both modes.
+ * bps_sketch_mode — the mode of a BlockPerm-SJLT handle (negative for NULL / FlashBlockRow).
+ */
+int bps_make_sketch_ex(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t s, uint64_t seed,
+                       int mode, bps_sketch** out);
+int bps_sketch_mode(const bps_sketch* sk);
 
 /*
  * FlashBlockRow (Alg. alg:blockrowsketch P:1447-1464) — the

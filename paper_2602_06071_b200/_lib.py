@@ -64,6 +64,10 @@ def _load() -> ctypes.CDLL:
     L.bps_apply_adjoint.restype = ctypes.c_int
     L.bps_apply_adjoint_ex.argtypes = [vp, vp, i64, i64, vp, i64, vp, ctypes.c_int]
     L.bps_apply_adjoint_ex.restype = ctypes.c_int
+    L.bps_make_sketch_ex.argtypes = [i64, i64, i64, i32, i32, u64, ctypes.c_int, ctypes.POINTER(vp)]
+    L.bps_make_sketch_ex.restype = ctypes.c_int
+    L.bps_sketch_mode.argtypes = [vp]
+    L.bps_sketch_mode.restype = ctypes.c_int
     L.bps_make_blockrow.argtypes = [i64, i64, i64, i32, i32, u64, ctypes.POINTER(vp)]
     L.bps_make_blockrow.restype = ctypes.c_int
     L.bps_blockrow_neighbors.argtypes = [vp, i64, ctypes.POINTER(i32)]

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) bps_adjoint_tc_kernel(const AdjAr
       {
         uint4* bz = reinterpret_cast<uint4*>(smem + args.off_band);
         for (uint32_t i = bt; i < (uint32_t)NB * BT / 16; i += kBandT) bz[i] = make_uint4(0, 0, 0, 0);
-        for (uint32_t c = bt; c < ncombo; c += kBandT) crow[c] = (c / p.s) * p.B_r + (c % p.s) * p.C;
+        for (uint32_t c = bt; c < ncombo; c += kBandT) crow[c] = band_crow(p, c / p.s, c % p.s);
       }
       uint32_t prev[NB][4];  // rows written NB stages ago (this buffer), 8 bits each (κ·B_r ≤ 256)
 #pragma unroll
@@ -212,14 +212,23 @@ __global__ void __launch_bounds__(kThreads, 1) bps_adjoint_tc_kernel(const AdjAr
             const uint32_t sig = c / p.s, j = c % p.s;
             const uint32_t ell = mod_pos(q - (int64_t)sig - 1, kappa) + 1;
             const uint32_t g = affine_pow(p, (uint64_t)mod_pos(q - (int64_t)ell, p.M), 0u);
-            ck[c] = (((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | (uint64_t)j) ^ p.K;
+            ck[c] = (((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | (uint64_t)band_jfield(p, j)) ^ p.K;
           }
           ptx::named_bar_sync(1, kBandT);
         }
         const uint64_t uk = (uint64_t)((uint32_t)kc * kU + u) << 8;
         const uint32_t sbase = band_u32 + bs * BT;
-        const bool clear = local_no >= NB;
+        bool clear = local_no >= NB;
         ++local_no;
+        if (p.mode && clear) {  // AffineUnique: clear every stale entry before any thread writes (see bps_tc.cu)
+#pragma unroll
+          for (int w = 0; w < 4; ++w)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if ((uint32_t)(4 * w + i) < T) ptx::st_shared_u16(entry(sbase, (prev[0][w] >> (8 * i)) & 0xFFu), 0);
+          ptx::named_bar_sync(3, kBandT);
+          clear = false;
+        }
         uint32_t nw[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
@@ -236,8 +245,9 @@ __global__ void __launch_bounds__(kThreads, 1) bps_adjoint_tc_kernel(const AdjAr
               if (t >= T) break;
               const uint32_t c = g4 + 4 * t;
               if (clear) ptx::st_shared_u16(entry(sbase, (prev[0][w] >> (8 * i)) & 0xFFu), 0);
-              const uint32_t rho = crow[c] + __umulhi((uint32_t)(z[i] >> 32), p.C);  // R3
-              ptx::st_shared_u16(entry(sbase, rho), (z[i] & 1) ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
+              uint32_t neg;
+              const uint32_t rho = band_draw(p, crow[c], z[i], neg);
+              ptx::st_shared_u16(entry(sbase, rho), neg ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
               nw[w] |= rho << (8 * i);
             }
           }

@@ -142,16 +142,22 @@ uint64_t bps_kernel_launches(void) { return g_launches.load(); }
 
 const char* bps_version(void) { return "bps 0.1 sm_100a (sparse gather + tcgen05 NT band kernel)"; }
 
-int bps_make_sketch(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t s, uint64_t seed, bps_sketch** out) {
+int bps_make_sketch_ex(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t s, uint64_t seed, int mode,
+                       bps_sketch** out) {
   if (!out) return fail(BPS_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
+  if (mode != BPS_MODE_ROWPART && mode != BPS_MODE_AFFINE) return fail(BPS_ERR_INVALID_ARG, "unknown intra-block mode");
   if (M < 1 || B_r < 1 || B_c < 1) return fail(BPS_ERR_INVALID_ARG, "M, B_r, B_c must be >= 1");
   if (M >= (int64_t(1) << 24)) return fail(BPS_ERR_INVALID_ARG, "M must be < 2^24 (counter field, R2)");
   if (B_c >= (int64_t(1) << 24)) return fail(BPS_ERR_INVALID_ARG, "B_c must be < 2^24 (counter field, R2)");
   if (B_r >= (int64_t(1) << 31)) return fail(BPS_ERR_INVALID_ARG, "B_r too large");
   if (kappa < 1 || kappa > M || kappa > 256) return fail(BPS_ERR_INVALID_ARG, "need 1 <= kappa <= min(M, 256) (P:1531)");
-  if (s < 1 || s > B_r || s > 256 || B_r % s != 0)
+  if (mode == BPS_MODE_AFFINE) {
+    if ((B_r & (B_r - 1)) != 0 || B_r > 65536 || s < 1 || s > B_r || s > 32)
+      return fail(BPS_ERR_INVALID_ARG, "AffineUnique: B_r a power of two <= 2^16 and 1 <= s <= min(B_r, 32) (R18)");
+  } else if (s < 1 || s > B_r || s > 256 || B_r % s != 0) {
     return fail(BPS_ERR_INVALID_ARG, "need 1 <= s <= min(B_r, 256) and B_r % s == 0 (row-partitioned, R1)");
+  }
   if (M > (int64_t(1) << 62) / B_c || M > (int64_t(1) << 62) / B_r) return fail(BPS_ERR_OVERFLOW, "M*B_c or M*B_r overflows");
   bps_sketch* sk = new (std::nothrow) bps_sketch;
   if (!sk) return fail(BPS_ERR_INVALID_ARG, "out of host memory");
@@ -172,12 +178,23 @@ int bps_make_sketch(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t 
   p.kappa = (uint32_t)kappa;
   p.s = (uint32_t)s;
   p.C = (uint32_t)(B_r / s);
+  p.mode = (uint32_t)mode;
+  p.Brmask = (uint32_t)(B_r - 1);
   p.Mmask = ((M & (M - 1)) == 0) ? (uint32_t)(M - 1) : 0u;
   select_affine(seed, (uint64_t)M, &p.a, &p.b);
   p.K = mix64(seed ^ kTagPhi);
   p.scale = (float)(1.0 / std::sqrt((double)kappa * (double)s));
   *out = sk;
   return BPS_OK;
+}
+
+int bps_make_sketch(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t s, uint64_t seed, bps_sketch** out) {
+  return bps_make_sketch_ex(M, B_r, B_c, kappa, s, seed, BPS_MODE_ROWPART, out);
+}
+
+int bps_sketch_mode(const bps_sketch* sk) {
+  if (!sk) return fail(BPS_ERR_INVALID_ARG, "sketch handle is NULL");
+  return sk->kind == 0 ? (int)sk->p.mode : fail(BPS_ERR_INVALID_ARG, "not a BlockPerm-SJLT sketch");
 }
 
 int bps_make_blockrow(int64_t M, int64_t B_r, int64_t B_c, int32_t kappa, int32_t s, uint64_t seed,

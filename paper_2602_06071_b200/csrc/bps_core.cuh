@@ -34,6 +34,8 @@ struct SketchParams {
   uint32_t a, b;                      // f(x) = (a x + b) mod M   (R4)
   uint64_t K;                         // mix64(seed ^ kTagPhi)     (R2)
   float scale;                        // fp32(1/sqrt(kappa*s))     (R6)
+  uint32_t mode;                      // 0: row-partitioned (R1, R3); 1: AffineUnique (R18)
+  uint32_t Brmask;                    // B_r - 1 (mode 1: B_r is a power of two)
 };
 
 // f(x) = (a x + b) mod M.
@@ -91,9 +93,37 @@ BPS_HD Draw draw_from_hash(const SketchParams& p, uint64_t z, uint32_t j) {
   return Draw{j * p.C + off, (uint32_t)(z & 1)};
 }
 
+// AffineUnique (R18): z = hash of (g, ℓ, u) with j-field 0; α odd, β a shift;
+// row_j = (α·j + β) mod B_r, sign_j = bit j of z.
+BPS_HD Draw affine_draw(const SketchParams& p, uint64_t z, uint32_t j) {
+  const uint32_t alpha = (uint32_t)(((((z >> 32) & 0xFFFFu) * p.B_r) >> 16) | 1u);
+  const uint32_t beta = (uint32_t)(((z >> 48) * p.B_r) >> 16);
+  return Draw{(alpha * j + beta) & p.Brmask, (uint32_t)((z >> j) & 1u)};
+}
+
 BPS_HD Draw pattern(const SketchParams& p, uint32_t g, uint32_t ell, uint32_t u, uint32_t j) {
+  if (p.mode) return affine_draw(p, pattern_hash(p, g, ell, u, 0), j);
   return draw_from_hash(p, pattern_hash(p, g, ell, u, j), j);
 }
+
+#ifdef __CUDACC__
+// Band generators (tc kernels): combo c = (σ, j) of a block has a precomputed key
+// ck = (g≪40 | (ℓ−1)≪32 | jfield) ⊕ K with jfield = j (mode 0) or 0 (mode 1), and
+// cr = band_crow(...); z = mix64(ck ⊕ u≪8).  Returns the band row ρ and the sign bit.
+__host__ __device__ __forceinline__ uint32_t band_jfield(const SketchParams& p, uint32_t j) { return p.mode ? 0u : j; }
+__host__ __device__ __forceinline__ uint32_t band_crow(const SketchParams& p, uint32_t sigma, uint32_t j) {
+  return p.mode ? (sigma * p.B_r) | (j << 16) : sigma * p.B_r + j * p.C;
+}
+__device__ __forceinline__ uint32_t band_draw(const SketchParams& p, uint32_t cr, uint64_t z, uint32_t& neg) {
+  if (p.mode) {
+    const Draw d = affine_draw(p, z, cr >> 16);
+    neg = d.neg;
+    return (cr & 0xFFFFu) + d.row;
+  }
+  neg = (uint32_t)(z & 1u);
+  return cr + __umulhi((uint32_t)(z >> 32), p.C);  // R3
+}
+#endif
 
 // ---------------------------------------------------------------- FlashBlockRow (R14-R16)
 struct BlockRowParams {

@@ -39,11 +39,23 @@ class Sketch:
     """BlockPerm-SJLT S (k×d, k = M·B_r, d = M·B_c) regenerated on the fly (bps_make_sketch);
     kind="blockrow": the FlashBlockRow sampling sketch of P:1424-1466 (bps_make_blockrow)."""
 
-    def __init__(self, M: int, B_r: int, B_c: int, kappa: int, s: int, seed: int = 0, kind: str = "blockperm"):
+    MODES = {"rowpart": 0, "affine": 1}
+
+    def __init__(self, M: int, B_r: int, B_c: int, kappa: int, s: int, seed: int = 0, kind: str = "blockperm",
+                 mode: str = "rowpart"):
+        """kind: "blockperm" (BlockPerm-SJLT) or "blockrow" (FlashBlockRow); mode (blockperm only):
+        "rowpart" (R1) or "affine" (AffineUnique, R18)."""
         h = ctypes.c_void_p()
-        make = {"blockperm": lib.bps_make_sketch, "blockrow": lib.bps_make_blockrow}[kind]
-        check(make(M, B_r, B_c, kappa, s, ctypes.c_uint64(seed & (2**64 - 1)), ctypes.byref(h)))
-        self.kind = kind
+        sd = ctypes.c_uint64(seed & (2**64 - 1))
+        if kind == "blockperm":
+            check(lib.bps_make_sketch_ex(M, B_r, B_c, kappa, s, sd, self.MODES[mode], ctypes.byref(h)))
+        elif kind == "blockrow":
+            if mode != "rowpart":
+                raise ValueError("mode applies to BlockPerm-SJLT sketches only")
+            check(lib.bps_make_blockrow(M, B_r, B_c, kappa, s, sd, ctypes.byref(h)))
+        else:
+            raise ValueError(f"unknown sketch kind {kind!r}")
+        self.kind, self.mode = kind, mode
         self._h = h
         self.M, self.B_r, self.B_c, self.kappa, self.s, self.seed = M, B_r, B_c, kappa, s, seed & (2**64 - 1)
         d, k = ctypes.c_int64(), ctypes.c_int64()

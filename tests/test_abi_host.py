@@ -145,3 +145,25 @@ def test_blockrow_validation_and_unsupported_calls():
     assert lib.bps_sketch_kind(bp.handle) == 0
     with pytest.raises(BpsError):
         bp.neighbors_row(0)
+
+
+def test_affine_mode_host_draws_match_oracle():
+    """AffineUnique (R18): libbps's (row, sign) draws equal the oracle's bit-exactly."""
+    import numpy as np
+
+    import oracle
+
+    for layout, seed in [((8, 32, 128, 2, 2), 1), ((128, 32, 8192, 4, 4), 1234), ((16, 64, 128, 4, 8), 9)]:
+        sk = Sketch(*layout, seed=seed, mode="affine")
+        osk = oracle.make_sketch(*layout, seed=seed, mode="affine")
+        assert lib.bps_sketch_mode(sk.handle) == 1
+        assert lib.bps_sketch_mode(Sketch(*layout, seed=seed).handle) == 0
+        rng = np.random.default_rng(1)
+        for _ in range(200):
+            g, ell = int(rng.integers(osk.M)), int(rng.integers(1, osk.kappa + 1))
+            u, j = int(rng.integers(osk.B_c)), int(rng.integers(osk.s))
+            assert sk.pattern(g, ell, u, j) == oracle.pattern(osk, g, ell, u, j)
+    for args in [(8, 24, 16, 2, 2), (8, 64, 16, 2, 33)]:
+        with pytest.raises(BpsError) as e:
+            Sketch(*args, seed=0, mode="affine")
+        assert e.value.code == -1

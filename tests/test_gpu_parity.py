@@ -44,8 +44,8 @@ def _run(sk, A_host, variant, dtype=torch.float32, transposed=False):
     return Y.cpu().numpy()
 
 
-def _pair(M, Br, Bc, kappa, s, seed=1234):
-    return Sketch(M, Br, Bc, kappa, s, seed), oracle.make_sketch(M, Br, Bc, kappa, s, seed)
+def _pair(M, Br, Bc, kappa, s, seed=1234, mode="rowpart"):
+    return Sketch(M, Br, Bc, kappa, s, seed, mode=mode), oracle.make_sketch(M, Br, Bc, kappa, s, seed, mode=mode)
 
 
 # ------------------------------------------------------------ bit-exact pattern
@@ -181,13 +181,13 @@ def test_deterministic(variant):
 
 
 # ------------------------------------------------- full-size configs, sampled outputs
-def _sampled_check(cfg, variant, kind="gaussian", n_cols=6, n_blocks=3, transposed=False):
+def _sampled_check(cfg, variant, kind="gaussian", n_cols=6, n_blocks=3, transposed=False, mode="rowpart"):
     """Full-size apply in the bench's launch configuration; the oracle recomputes a
     sample of output blocks × columns one by one (task contract ③)."""
     dev = torch.device("cuda")
     tdt = torch.float32 if cfg.dtype == "f32" else torch.bfloat16
-    sk = Sketch(**cfg.sketch_args())
-    osk = oracle.make_sketch(cfg.M, cfg.B_r, cfg.B_c, cfg.kappa, cfg.s, cfg.seed)
+    sk = Sketch(**cfg.sketch_args(), mode=mode)
+    osk = oracle.make_sketch(cfg.M, cfg.B_r, cfg.B_c, cfg.kappa, cfg.s, cfg.seed, mode=mode)
     A = synth.device_matrix(kind, cfg.d, cfg.n, seed=11, M=cfg.M, dtype=tdt)
     try:
         if transposed:
