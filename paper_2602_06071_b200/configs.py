@@ -60,5 +60,14 @@ def sweep(kappa: int, s: int, dtype: str = "bf16") -> Config:
     return Config(f"sweep_k{kappa}_s{s}_{dtype}", d=1 << 22, k=4096, kappa=kappa, s=s, n=1024, dtype=dtype, B_r=32)
 
 
+def sweep_tuned(kappa: int, s: int, dtype: str = "bf16") -> Config:
+    """The same sweep point with B_r chosen per (κ, s) by the production layout rule
+    B_r = 128/κ clamped to [max(s, 8), 64] (the paper tunes B_r per shape from a menu of
+    templates): κ·B_r = 128 for κ ≥ 2, one band tile of the tcgen05 kernel."""
+    B_r = min(64, max(max(s, 8), 128 // kappa))
+    return Config(f"sweepT_k{kappa}_s{s}_{dtype}", d=1 << 22, k=4096, kappa=kappa, s=s, n=1024, dtype=dtype, B_r=B_r)
+
+
 SWEEP = [sweep(k, s, dt) for dt in ("bf16", "f32") for k in (1, 2, 4, 8, 16) for s in (1, 2, 4, 8)]
-CONFIGS = {c.name: c for c in [TINY, LS, GRAD, SMALLN, SCALEOUT] + SWEEP}
+SWEEP_TUNED = [sweep_tuned(k, s, dt) for dt in ("bf16", "f32") for k in (1, 2, 4, 8, 16) for s in (1, 2, 4, 8)]
+CONFIGS = {c.name: c for c in [TINY, LS, GRAD, SMALLN, SCALEOUT] + SWEEP + SWEEP_TUNED}

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <string>
+#include <type_traits>
 
 #include "bps_internal.h"
 #include "bps_ptx.cuh"
@@ -175,93 +176,100 @@ __global__ void __launch_bounds__(kThreads, 1) bps_adjoint_tc_kernel(const AdjAr
         if (++kc == nk) kc = 0, ++q, h = affine_step(p, h);
       }
     } else if (warp < kWConv) {
-      // ===================== band generator (same stages as the forward kernel) =====================
-      // Thread (u, g4) owns column u of every band stage for the row chunks c = g4 + 4t,
-      // c = σ·s + j; it clears the entry it wrote NB stages ago instead of zero-filling.
-      const int bt = threadIdx.x - kWBand * 32;
-      const uint32_t u = (uint32_t)bt & (kU - 1);
-      const uint32_t g4 = (uint32_t)bt >> 6;
-      const uint32_t ncombo = kappa * p.s;
-      const uint32_t T = ncombo > g4 ? (ncombo - g4 + 3) / 4 : 0;  // ≤ 16 (κ·s ≤ 64)
-      const uint32_t band_u32 = ptx::smem_u32(smem + args.off_band);
-      const uint32_t ucol = u >> 3, ulo = (u & 7) * 2;
-      auto entry = [&](uint32_t sbase, uint32_t rho) {
-        return sbase + (rho >> 3) * 1024 + (rho & 7) * 128 + ((ucol ^ (rho & 7)) << 4) + ulo;
+      auto band_gen = [&](auto affine_tag) {  // specialised on the intra-block mode
+        constexpr bool AFF = decltype(affine_tag)::value;
+        // ===================== band generator (same stages as the forward kernel) =====================
+        // Thread (u, g4) owns column u of every band stage for the row chunks c = g4 + 4t,
+        // c = σ·s + j; it clears the entry it wrote NB stages ago instead of zero-filling.
+        const int bt = threadIdx.x - kWBand * 32;
+        const uint32_t u = (uint32_t)bt & (kU - 1);
+        const uint32_t g4 = (uint32_t)bt >> 6;
+        const uint32_t ncombo = kappa * p.s;
+        const uint32_t T = ncombo > g4 ? (ncombo - g4 + 3) / 4 : 0;  // ≤ 16 (κ·s ≤ 64)
+        const uint32_t band_u32 = ptx::smem_u32(smem + args.off_band);
+        const uint32_t ucol = u >> 3, ulo = (u & 7) * 2;
+        auto entry = [&](uint32_t sbase, uint32_t rho) {
+          return sbase + (rho >> 3) * 1024 + (rho & 7) * 128 + ((ucol ^ (rho & 7)) << 4) + ulo;
+        };
+        {
+          uint4* bz = reinterpret_cast<uint4*>(smem + args.off_band);
+          for (uint32_t i = bt; i < (uint32_t)NB * BT / 16; i += kBandT) bz[i] = make_uint4(0, 0, 0, 0);
+          for (uint32_t c = bt; c < ncombo; c += kBandT) crow[c] = band_crow(p, c / p.s, c % p.s);
+        }
+        uint32_t prev[NB][4];  // rows written NB stages ago (this buffer), 8 bits each (κ·B_r ≤ 256)
+  #pragma unroll
+        for (int b = 0; b < NB; ++b)
+  #pragma unroll
+          for (int w = 0; w < 4; ++w) prev[b][w] = 0;
+        int bs = 0;
+        uint32_t bph = 0;
+        int64_t local_no = 0;
+        int kc = (int)(S0 % nk);
+        int64_t q = S0 / nk;
+        for (int64_t st = S0; st < S1; ++st, q += (kc + 1 == nk), kc = (kc + 1 == nk) ? 0 : kc + 1) {
+          uint64_t* ck = ckey + (q & 1) * 64;
+          ptx::mbar_wait_sleep(&band_empty[bs], bph ^ 1, 20);
+          if (kc == 0 || st == S0) {
+            // input block q: the output i ≡ σ (mod κ) feeding it is i = q - ℓ, ℓ = ((q - σ - 1) mod κ) + 1
+            for (uint32_t c = bt; c < ncombo; c += kBandT) {
+              const uint32_t sig = c / p.s, j = c % p.s;
+              const uint32_t ell = mod_pos(q - (int64_t)sig - 1, kappa) + 1;
+              const uint32_t g = affine_pow(p, (uint64_t)mod_pos(q - (int64_t)ell, p.M), 0u);
+              ck[c] = (((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | (uint64_t)band_jfield(p, j)) ^ p.K;
+            }
+            ptx::named_bar_sync(1, kBandT);
+          }
+          const uint64_t uk = (uint64_t)((uint32_t)kc * kU + u) << 8;
+          const uint32_t sbase = band_u32 + bs * BT;
+          bool clear = local_no >= NB;
+          ++local_no;
+          if (AFF && clear) {  // AffineUnique: clear every stale entry before any thread writes (see bps_tc.cu)
+  #pragma unroll
+            for (int w = 0; w < 4; ++w)
+  #pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if ((uint32_t)(4 * w + i) < T) ptx::st_shared_u16(entry(sbase, (prev[0][w] >> (8 * i)) & 0xFFu), 0);
+            ptx::named_bar_sync(3, kBandT);
+            clear = false;
+          }
+          uint32_t nw[4] = {0, 0, 0, 0};
+  #pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            if ((uint32_t)w * 4 < T) {
+              uint64_t z[4];
+  #pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const uint32_t c = g4 + 4 * (4 * w + i);
+                z[i] = mix64(ck[c < ncombo ? c : g4] ^ uk);
+              }
+  #pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const uint32_t t = 4 * w + i;
+                if (t >= T) break;
+                const uint32_t c = g4 + 4 * t;
+                if (clear) ptx::st_shared_u16(entry(sbase, (prev[0][w] >> (8 * i)) & 0xFFu), 0);
+                uint32_t neg;
+                const uint32_t rho = band_draw_t<AFF>(p, crow[c], z[i], neg);
+                ptx::st_shared_u16(entry(sbase, rho), neg ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
+                nw[w] |= rho << (8 * i);
+              }
+            }
+          }
+  #pragma unroll
+          for (int b = 0; b + 1 < NB; ++b)
+  #pragma unroll
+            for (int w = 0; w < 4; ++w) prev[b][w] = prev[b + 1][w];
+  #pragma unroll
+          for (int w = 0; w < 4; ++w) prev[NB - 1][w] = nw[w];
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive(&band_full[bs]);
+          if (++bs == NB) bs = 0, bph ^= 1;
+        }
       };
-      {
-        uint4* bz = reinterpret_cast<uint4*>(smem + args.off_band);
-        for (uint32_t i = bt; i < (uint32_t)NB * BT / 16; i += kBandT) bz[i] = make_uint4(0, 0, 0, 0);
-        for (uint32_t c = bt; c < ncombo; c += kBandT) crow[c] = band_crow(p, c / p.s, c % p.s);
-      }
-      uint32_t prev[NB][4];  // rows written NB stages ago (this buffer), 8 bits each (κ·B_r ≤ 256)
-#pragma unroll
-      for (int b = 0; b < NB; ++b)
-#pragma unroll
-        for (int w = 0; w < 4; ++w) prev[b][w] = 0;
-      int bs = 0;
-      uint32_t bph = 0;
-      int64_t local_no = 0;
-      int kc = (int)(S0 % nk);
-      int64_t q = S0 / nk;
-      for (int64_t st = S0; st < S1; ++st, q += (kc + 1 == nk), kc = (kc + 1 == nk) ? 0 : kc + 1) {
-        uint64_t* ck = ckey + (q & 1) * 64;
-        ptx::mbar_wait_sleep(&band_empty[bs], bph ^ 1, 20);
-        if (kc == 0 || st == S0) {
-          // input block q: the output i ≡ σ (mod κ) feeding it is i = q - ℓ, ℓ = ((q - σ - 1) mod κ) + 1
-          for (uint32_t c = bt; c < ncombo; c += kBandT) {
-            const uint32_t sig = c / p.s, j = c % p.s;
-            const uint32_t ell = mod_pos(q - (int64_t)sig - 1, kappa) + 1;
-            const uint32_t g = affine_pow(p, (uint64_t)mod_pos(q - (int64_t)ell, p.M), 0u);
-            ck[c] = (((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | (uint64_t)band_jfield(p, j)) ^ p.K;
-          }
-          ptx::named_bar_sync(1, kBandT);
-        }
-        const uint64_t uk = (uint64_t)((uint32_t)kc * kU + u) << 8;
-        const uint32_t sbase = band_u32 + bs * BT;
-        bool clear = local_no >= NB;
-        ++local_no;
-        if (p.mode && clear) {  // AffineUnique: clear every stale entry before any thread writes (see bps_tc.cu)
-#pragma unroll
-          for (int w = 0; w < 4; ++w)
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if ((uint32_t)(4 * w + i) < T) ptx::st_shared_u16(entry(sbase, (prev[0][w] >> (8 * i)) & 0xFFu), 0);
-          ptx::named_bar_sync(3, kBandT);
-          clear = false;
-        }
-        uint32_t nw[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          if ((uint32_t)w * 4 < T) {
-            uint64_t z[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint32_t c = g4 + 4 * (4 * w + i);
-              z[i] = mix64(ck[c < ncombo ? c : g4] ^ uk);
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint32_t t = 4 * w + i;
-              if (t >= T) break;
-              const uint32_t c = g4 + 4 * t;
-              if (clear) ptx::st_shared_u16(entry(sbase, (prev[0][w] >> (8 * i)) & 0xFFu), 0);
-              uint32_t neg;
-              const uint32_t rho = band_draw(p, crow[c], z[i], neg);
-              ptx::st_shared_u16(entry(sbase, rho), neg ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
-              nw[w] |= rho << (8 * i);
-            }
-          }
-        }
-#pragma unroll
-        for (int b = 0; b + 1 < NB; ++b)
-#pragma unroll
-          for (int w = 0; w < 4; ++w) prev[b][w] = prev[b + 1][w];
-#pragma unroll
-        for (int w = 0; w < 4; ++w) prev[NB - 1][w] = nw[w];
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&band_full[bs]);
-        if (++bs == NB) bs = 0, bph ^= 1;
-      }
+      if (p.mode)
+        band_gen(std::true_type{});
+      else
+        band_gen(std::false_type{});
     } else if (warp < kWMma) {
       // ===================== window converter: Y rows -> (hi, lo) bf16, SW128 MN-major =====================
       const int ct = threadIdx.x - kWConv * 32;

@@ -114,6 +114,17 @@ __host__ __device__ __forceinline__ uint32_t band_jfield(const SketchParams& p, 
 __host__ __device__ __forceinline__ uint32_t band_crow(const SketchParams& p, uint32_t sigma, uint32_t j) {
   return p.mode ? (sigma * p.B_r) | (j << 16) : sigma * p.B_r + j * p.C;
 }
+template <bool AFF>
+__device__ __forceinline__ uint32_t band_draw_t(const SketchParams& p, uint32_t cr, uint64_t z, uint32_t& neg) {
+  if constexpr (AFF) {
+    const Draw d = affine_draw(p, z, cr >> 16);
+    neg = d.neg;
+    return (cr & 0xFFFFu) + d.row;
+  } else {
+    neg = (uint32_t)(z & 1u);
+    return cr + __umulhi((uint32_t)(z >> 32), p.C);  // R3
+  }
+}
 __device__ __forceinline__ uint32_t band_draw(const SketchParams& p, uint32_t cr, uint64_t z, uint32_t& neg) {
   if (p.mode) {
     const Draw d = affine_draw(p, z, cr >> 16);

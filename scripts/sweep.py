@@ -30,7 +30,11 @@ def timed(fn, reps):
 
 
 def main():
-    dtypes = sys.argv[1:] or ["bf16", "f32"]
+    args = sys.argv[1:]
+    tuned = "--tuned" in args  # B_r per (κ, s) by the layout rule (configs.sweep_tuned)
+    variants = ("tc",) if "--tc-only" in args else ("sparse", "tc")
+    dtypes = [a for a in args if not a.startswith("--")] or ["bf16", "f32"]
+    make = C.sweep_tuned if tuned else C.sweep
     for dt in dtypes:
         base = C.sweep(1, 1, dt)
         tdt = torch.float32 if dt == "f32" else torch.bfloat16
@@ -38,10 +42,10 @@ def main():
         Y = torch.empty((base.k, base.n), device="cuda")
         for kappa in (1, 2, 4, 8, 16):
             for s in (1, 2, 4, 8):
-                cfg = C.sweep(kappa, s, dt)
+                cfg = make(kappa, s, dt)
                 sk = Sketch(**cfg.sketch_args())
-                for variant in ("sparse", "tc"):
-                    rec = {"dtype": dt, "kappa": kappa, "s": s, "variant": variant, "config": cfg.name}
+                for variant in variants:
+                    rec = {"dtype": dt, "kappa": kappa, "s": s, "B_r": cfg.B_r, "variant": variant, "config": cfg.name}
                     try:
                         fn = lambda: sk.apply(A, out=Y, variant=variant)  # noqa: E731
                         fn()

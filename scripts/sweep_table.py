@@ -1,20 +1,29 @@
-"""Render gpurun_out/sweep.jsonl (scripts/sweep.py) as a markdown table of % of measured HBM peak."""
-import json, sys
+"""Render a scripts/sweep.py JSONL file as markdown tables (GB/s and % of the measured HBM peak).
+Variants absent from the file are omitted; B_r is taken from the records (fixed 32 or tuned)."""
+import json
+import sys
+
 rows = [json.loads(l) for l in open(sys.argv[1]) if l.strip()]
+variants = [v for v in ("sparse", "tc") if any(r["variant"] == v for r in rows)]
 out = []
 for dt in ("bf16", "f32"):
-    out.append(f"\n### {dt} input (d=2^22, k=4096, n=1024, B_r=32) — GB/s (% of 6545 GB/s measured copy peak)\n")
-    out.append("| κ \\\\ s | " + " | ".join(f"s={s} sparse | s={s} tc" for s in (1, 2, 4, 8)) + " |")
-    out.append("|---|" + "---|" * 8)
+    sel = [r for r in rows if r["dtype"] == dt]
+    if not sel:
+        continue
+    brs = sorted({r.get("B_r", 32) for r in sel})
+    br_txt = f"B_r={brs[0]}" if len(brs) == 1 else "B_r tuned per κ (clamp(128/κ, max(s,8), 64))"
+    out.append(f"\n### {dt} input (d=2^22, k=4096, n=1024, {br_txt}) — GB/s (% of 6545 GB/s measured copy peak)\n")
+    out.append("| κ \\\\ s | " + " | ".join(f"s={s} {v}" for s in (1, 2, 4, 8) for v in variants) + " |")
+    out.append("|---|" + "---|" * (4 * len(variants)))
     for k in (1, 2, 4, 8, 16):
         cells = []
         for s in (1, 2, 4, 8):
-            for v in ("sparse", "tc"):
-                r = next((x for x in rows if x["dtype"] == dt and x["kappa"] == k and x["s"] == s and x["variant"] == v), None)
+            for v in variants:
+                r = next((x for x in sel if x["kappa"] == k and x["s"] == s and x["variant"] == v), None)
                 if r is None:
                     cells.append("—")
                 elif "gbs" in r:
-                    cells.append(f"{r['gbs']:.0f} ({100*r['frac']:.0f}%)")
+                    cells.append(f"{r['gbs']:.0f} ({100*r['frac']:.0f}%)" + (f" B_r={r['B_r']}" if len(brs) > 1 and v == variants[-1] else ""))
                 else:
                     cells.append("n/a")
         out.append(f"| κ={k} | " + " | ".join(cells) + " |")

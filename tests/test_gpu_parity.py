@@ -232,7 +232,9 @@ def test_grad_config_sampled(variant):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("cfg", [C.sweep(1, 1), C.sweep(4, 8), C.sweep(16, 2), C.sweep(8, 4, "f32")],
+@pytest.mark.parametrize("cfg", [C.sweep(1, 1), C.sweep(4, 8), C.sweep(16, 2), C.sweep(8, 4, "f32"),
+                                 C.sweep_tuned(16, 8), C.sweep_tuned(16, 1, "f32"), C.sweep_tuned(8, 8),
+                                 C.sweep_tuned(1, 8, "f32")],
                          ids=lambda c: c.name)
 def test_sweep_sampled(cfg):
     _sampled_check(cfg, "auto")
