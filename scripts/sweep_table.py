@@ -4,7 +4,7 @@ import json
 import sys
 
 rows = [json.loads(l) for l in open(sys.argv[1]) if l.strip()]
-variants = [v for v in ("sparse", "tc") if any(r["variant"] == v for r in rows)]
+variants = [v for v in ("sparse", "tc", "auto") if any(r["variant"] == v for r in rows)]
 out = []
 for dt in ("bf16", "f32"):
     sel = [r for r in rows if r["dtype"] == dt]
