@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1) bps_adjoint_tc_kernel(const AdjAr
         const uint32_t band_u32 = ptx::smem_u32(smem + args.off_band);
         const uint32_t ucol = u >> 3, ulo = (u & 7) * 2;
         auto entry = [&](uint32_t sbase, uint32_t rho) {
-          return sbase + (rho >> 3) * 1024 + (rho & 7) * 128 + ((ucol ^ (rho & 7)) << 4) + ulo;
+          return sbase + rho * 128 + (((rho ^ ucol) & 7) << 4) + ulo;  // SW128 row ρ
         };
         {
           uint4* bz = reinterpret_cast<uint4*>(smem + args.off_band);
