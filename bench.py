@@ -48,6 +48,7 @@ def parse():
                     help="blockrow: the FlashBlockRow sampling sketch (P:1424-1466); secondary line")
     ap.add_argument("--mode", default="rowpart", choices=["rowpart", "affine"],
                     help="intra-block pattern of BlockPerm-SJLT: row-partitioned (R1) or AffineUnique (R18)")
+    ap.add_argument("--panel-cols", type=int, default=0, help="scaleout: columns per HBM panel (0 = fit 60%% of free memory)")
     ap.add_argument("--no-workspace", action="store_true", help="block-aligned ranges (no balanced workspace)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -219,6 +220,23 @@ def main():
 
         def step():
             sk.apply_adjoint(Yin, out=X, variant=args.variant)
+    elif cfg.name == "scaleout":
+        # BASELINE configs[4]: the job's n columns are split over the ranks (strong scaling) and each
+        # rank streams its share through HBM in column panels that fit (2 TiB of A in total): every
+        # panel is a full apply over all d rows into its own column range of Y (ldy = n_rank).  The
+        # panel buffer is reused across panels (synthetic data), so each step reads d·n_rank·elem.
+        n = cfg.n // world
+        free = torch.cuda.mem_get_info(dev)[0]
+        n_p = args.panel_cols or max(128, min(n, int(0.6 * free) // (cfg.d * cfg.elem) // 128 * 128))
+        A = synth.device_matrix(args.kind, cfg.d, n_p, seed=1000 + rank, M=cfg.M, dtype=tdt, device=dev)
+        Y = torch.empty((cfg.k, n), dtype=torch.float32, device=dev)
+        panels = [(c0, min(n_p, n - c0)) for c0 in range(0, n, n_p)]
+        args.no_e2e = True  # 2 TiB of host->device traffic per step is not an end-to-end workload
+        args.panels = {"panel_cols": n_p, "panels_per_step": len(panels), "n_per_rank": n}
+
+        def step():
+            for c0, w in panels:
+                sk.apply(A[:, :w], out=Y[:, c0:c0 + w], variant=args.variant, use_workspace=not args.no_workspace)
     else:
         A = synth.device_matrix(args.kind, cfg.d, n, seed=1000 + rank, M=cfg.M, dtype=tdt, device=dev)
         Y = torch.empty((cfg.k, n), dtype=torch.float32, device=dev)
@@ -314,7 +332,7 @@ def main():
             "metric": ("blockrow_gather_gbs" if args.sketch == "blockrow" else METRIC) if args.op == "apply"
             else "adjoint_throughput_gbs", "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if block else "weak",
+            "scaling": "strong" if (block or cfg.name == "scaleout") else "weak",
             "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" or args.op == "adjoint" else "bf16-in/f32-acc",
             "data": f"synthetic {args.kind} (torch Philox on device), seed {1000}+rank",
             "config": {"workload": cfg.name, "d": cfg.d, "k": cfg.k, "kappa": cfg.kappa, "s": cfg.s,
@@ -323,6 +341,7 @@ def main():
                                        else f"column-shard x{world} (no collective)"),
                        "l2": "inputs larger than L2 (no flush needed)" if bytes_rank > (256 << 20) else "input fits L2"},
             "columns_per_s": (n if block else world * n) / (ms / 1e3),
+            **({"panels": args.panels} if getattr(args, "panels", None) else {}),
             "gbs_per_gpu": value / world,
             "frac_of_8tbs": value / world / 8000.0,
             "ms_min": min(per), "ms_median": statistics.median(per),
