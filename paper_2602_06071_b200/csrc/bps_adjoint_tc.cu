@@ -223,35 +223,56 @@ __global__ void __launch_bounds__(kThreads, 1) bps_adjoint_tc_kernel(const AdjAr
           const uint32_t sbase = band_u32 + bs * BT;
           bool clear = local_no >= NB;
           ++local_no;
-          if (AFF && clear) {  // AffineUnique: clear every stale entry before any thread writes (see bps_tc.cu)
-  #pragma unroll
-            for (int w = 0; w < 4; ++w)
-  #pragma unroll
-              for (int i = 0; i < 4; ++i)
-                if ((uint32_t)(4 * w + i) < T) ptx::st_shared_u16(entry(sbase, (prev[0][w] >> (8 * i)) & 0xFFu), 0);
-            ptx::named_bar_sync(3, kBandT);
-            clear = false;
-          }
           uint32_t nw[4] = {0, 0, 0, 0};
+          if constexpr (AFF) {
+            // AffineUnique (R18), slot-major as in bps_tc.cu: one hash per (σ, u), σ ≡ g4 (mod 4);
+            // κ > 16 slots: zero-fill the stage behind a barrier instead of tracking stale rows
+            const bool zero_fill = kappa > 16u;
+            if (zero_fill && clear) {
+              uint4* bz = reinterpret_cast<uint4*>(smem + args.off_band + bs * BT);
+              for (uint32_t i = bt; i < BT / 16; i += kBandT) bz[i] = make_uint4(0, 0, 0, 0);
+              ptx::named_bar_sync(3, kBandT);
+            }
+            if (zero_fill) clear = false;
   #pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            if ((uint32_t)w * 4 < T) {
-              uint64_t z[4];
-  #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const uint32_t c = g4 + 4 * (4 * w + i);
-                z[i] = mix64(ck[c < ncombo ? c : g4] ^ uk);
+            for (int t = 0; t < 16; ++t) {
+              const uint32_t sig = g4 + 4 * t;
+              if (sig >= kappa) break;
+              const uint32_t base = sig * p.B_r;
+              if (t < 4 && clear) {
+                const uint32_t w = prev[0][t & 3], a0 = w & 0xFFFFu;
+                uint32_t r = w >> 16;
+                for (uint32_t j = 0; j < p.s; ++j, r = (r + a0) & p.Brmask) ptx::st_shared_u16(entry(sbase, base + r), 0);
               }
+              const uint64_t z = mix64(ck[sig * p.s] ^ uk);
+              const uint32_t alpha = (uint32_t)(((((z >> 32) & 0xFFFFu) * p.B_r) >> 16) | 1u);
+              const uint32_t beta = (uint32_t)(((z >> 48) * p.B_r) >> 16);
+              uint32_t r = beta, zs = (uint32_t)z;
+              for (uint32_t j = 0; j < p.s; ++j, r = (r + alpha) & p.Brmask, zs >>= 1)
+                ptx::st_shared_u16(entry(sbase, base + r), (zs & 1u) ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
+              if (t < 4) nw[t & 3] = alpha | (beta << 16);
+            }
+          } else {
   #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const uint32_t t = 4 * w + i;
-                if (t >= T) break;
-                const uint32_t c = g4 + 4 * t;
-                if (clear) ptx::st_shared_u16(entry(sbase, (prev[0][w] >> (8 * i)) & 0xFFu), 0);
-                uint32_t neg;
-                const uint32_t rho = band_draw_t<AFF>(p, crow[c], z[i], neg);
-                ptx::st_shared_u16(entry(sbase, rho), neg ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
-                nw[w] |= rho << (8 * i);
+            for (int w = 0; w < 4; ++w) {
+              if ((uint32_t)w * 4 < T) {
+                uint64_t z[4];
+  #pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const uint32_t c = g4 + 4 * (4 * w + i);
+                  z[i] = mix64(ck[c < ncombo ? c : g4] ^ uk);
+                }
+  #pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const uint32_t t = 4 * w + i;
+                  if (t >= T) break;
+                  const uint32_t c = g4 + 4 * t;
+                  if (clear) ptx::st_shared_u16(entry(sbase, (prev[0][w] >> (8 * i)) & 0xFFu), 0);
+                  uint32_t neg;
+                  const uint32_t rho = band_draw_t<false>(p, crow[c], z[i], neg);
+                  ptx::st_shared_u16(entry(sbase, rho), neg ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
+                  nw[w] |= rho << (8 * i);
+                }
               }
             }
           }
