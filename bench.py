@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--mode", default="rowpart", choices=["rowpart", "affine"],
                     help="intra-block pattern of BlockPerm-SJLT: row-partitioned (R1) or AffineUnique (R18)")
     ap.add_argument("--panel-cols", type=int, default=0, help="scaleout: columns per HBM panel (0 = fit 60%% of free memory)")
+    ap.add_argument("--layout", default="n", choices=["n", "t"],
+                    help="t: transposed layout (bps_apply_t, §8a8): X = Aᵀ n×d row-major in, Yᵀ n×k out")
     ap.add_argument("--no-workspace", action="store_true", help="block-aligned ranges (no balanced workspace)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -240,6 +242,13 @@ def main():
         def step():
             for c0, w in panels:
                 sk.apply(A[:, :w], out=Y[:, c0:c0 + w], variant=args.variant, use_workspace=not args.no_workspace)
+    elif args.layout == "t":
+        X = synth.device_matrix(args.kind, n, cfg.d, seed=1000 + rank, dtype=tdt, device=dev)
+        Yt = torch.empty((n, cfg.k), dtype=torch.float32, device=dev)
+        args.no_e2e = True
+
+        def step():
+            sk.apply_t(X, out=Yt, variant=args.variant, use_workspace=not args.no_workspace)
     else:
         A = synth.device_matrix(args.kind, cfg.d, n, seed=1000 + rank, M=cfg.M, dtype=tdt, device=dev)
         Y = torch.empty((cfg.k, n), dtype=torch.float32, device=dev)
@@ -339,7 +348,7 @@ def main():
             "vs_baseline": None, "dtype": "f32" if cfg.dtype == "f32" or args.op == "adjoint" else "bf16-in/f32-acc",
             "data": f"synthetic {args.kind} (torch Philox on device), seed {1000}+rank",
             "config": {"workload": cfg.name, "d": cfg.d, "k": cfg.k, "kappa": cfg.kappa, "s": cfg.s,
-                       "n_per_gpu": n, "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c, "variant": args.variant, "op": args.op, "sketch": args.sketch, "mode": args.mode,
+                       "n_per_gpu": n, "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c, "variant": args.variant, "op": args.op, "sketch": args.sketch, "mode": args.mode, "layout": args.layout,
                        "parallelism": (f"orbit-block-shard x{world} + NCCL all_gather" if block
                                        else f"column-shard x{world} (no collective)"),
                        "l2": "inputs larger than L2 (no flush needed)" if bytes_rank > (256 << 20) else "input fits L2"},
