@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--panel-cols", type=int, default=0, help="scaleout: columns per HBM panel (0 = fit 60%% of free memory)")
     ap.add_argument("--layout", default="n", choices=["n", "t"],
                     help="t: transposed layout (bps_apply_t, §8a8): X = Aᵀ n×d row-major in, Yᵀ n×k out")
+    ap.add_argument("--t-pad", type=int, default=0, help=argparse.SUPPRESS)  # experiment: ldx = d + pad (transposed)
     ap.add_argument("--no-workspace", action="store_true", help="block-aligned ranges (no balanced workspace)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -243,7 +244,8 @@ def main():
             for c0, w in panels:
                 sk.apply(A[:, :w], out=Y[:, c0:c0 + w], variant=args.variant, use_workspace=not args.no_workspace)
     elif args.layout == "t":
-        X = synth.device_matrix(args.kind, n, cfg.d, seed=1000 + rank, dtype=tdt, device=dev)
+        X = synth.device_matrix(args.kind, n, cfg.d + args.t_pad, seed=1000 + rank, dtype=tdt, device=dev)
+        X = X[:, :cfg.d]
         Yt = torch.empty((n, cfg.k), dtype=torch.float32, device=dev)
         args.no_e2e = True
 

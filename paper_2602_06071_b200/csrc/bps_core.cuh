@@ -106,6 +106,25 @@ BPS_HD Draw pattern(const SketchParams& p, uint32_t g, uint32_t ell, uint32_t u,
   return draw_from_hash(p, pattern_hash(p, g, ell, u, j), j);
 }
 
+// mix64 of (H:L) ⊕ (0:x) — the band generators' case, where only the low word varies with the
+// input row u — from a per-key fold: L1 = L ⊕ (H≫1) absorbs the first xor-shift (whose input
+// high word is the constant H), P1 = H·C1lo (mod 2^32) is the constant cross term of the first
+// multiply.  Exactly mix64 (z≫33 of a 64-bit z is hi≫1 in the low word), in 32-bit operations.
+BPS_HD void mix64_fold_key(uint64_t key, uint32_t& L1, uint32_t& P1) {
+  const uint32_t H = (uint32_t)(key >> 32), L = (uint32_t)key;
+  L1 = L ^ (H >> 1);
+  P1 = H * 0xED558CCDu;
+}
+BPS_HD void mix64_folded(uint32_t L1, uint32_t P1, uint32_t x, uint32_t& hi, uint32_t& lo) {
+  const uint32_t l1 = L1 ^ x;
+  const uint64_t w = (uint64_t)l1 * 0xED558CCDu + ((uint64_t)P1 << 32);       // z *= C1 (low word × C1lo)
+  const uint32_t h2 = (uint32_t)(w >> 32) + l1 * 0xFF51AFD7u, l2 = (uint32_t)w;  // + low word × C1hi
+  const uint32_t l3 = l2 ^ (h2 >> 1);                                           // z ^= z >> 33
+  const uint64_t w2 = (uint64_t)l3 * 0x1A85EC53u;                               // z *= C2
+  hi = (uint32_t)(w2 >> 32) + h2 * 0x1A85EC53u + l3 * 0xC4CEB9FEu;
+  lo = (uint32_t)w2 ^ (hi >> 1);                                                 // z ^= z >> 33
+}
+
 #ifdef __CUDACC__
 // Band generators (tc kernels): combo c = (σ, j) of a block has a precomputed key
 // ck = (g≪40 | (ℓ−1)≪32 | jfield) ⊕ K with jfield = j (mode 0) or 0 (mode 1), and
