@@ -70,4 +70,8 @@ def sweep_tuned(kappa: int, s: int, dtype: str = "bf16") -> Config:
 
 SWEEP = [sweep(k, s, dt) for dt in ("bf16", "f32") for k in (1, 2, 4, 8, 16) for s in (1, 2, 4, 8)]
 SWEEP_TUNED = [sweep_tuned(k, s, dt) for dt in ("bf16", "f32") for k in (1, 2, 4, 8, 16) for s in (1, 2, 4, 8)]
-CONFIGS = {c.name: c for c in [TINY, LS, GRAD, SMALLN, SCALEOUT] + SWEEP + SWEEP_TUNED}
+# experiment shapes for the transposed layout: the sweep point κ=4 s=4 with short vectors (d = 2^17,
+# 256 KiB per bf16 vector) and many of them, same bytes as the sweep
+TPROBE = Config("tprobe", d=1 << 17, k=4096, kappa=4, s=4, n=32768, dtype="bf16", B_r=32)
+TPROBE2 = Config("tprobe2", d=1 << 19, k=4096, kappa=4, s=4, n=8192, dtype="bf16", B_r=32)
+CONFIGS = {c.name: c for c in [TINY, LS, GRAD, SMALLN, SCALEOUT, TPROBE, TPROBE2] + SWEEP + SWEEP_TUNED}
