@@ -126,8 +126,9 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_baseline(cfg, n_sample, repeats=2):
-    """Time the oracle as it stands on a bounded column sample (rank 0, N=1)."""
+def cpu_baseline(cfg, n_sample, min_seconds=10.0, max_repeats=8):
+    """Time the oracle as it stands on a bounded column sample (rank 0, N=1): repeated until about
+    min_seconds of CPU work (at least 2, at most max_repeats runs), median reported."""
     import numpy as np
 
     import oracle
@@ -136,12 +137,12 @@ def cpu_baseline(cfg, n_sample, repeats=2):
     osk = oracle.make_sketch(cfg.M, cfg.B_r, cfg.B_c, cfg.kappa, cfg.s, cfg.seed)
     A = synth.host_matrix("gaussian", cfg.d, n_sample, seed=3, dtype=np.float32)
     times = []
-    for _ in range(repeats):
+    while len(times) < 2 or (sum(times) < min_seconds and len(times) < max_repeats):
         t0 = time.perf_counter()
         oracle.apply(osk, A)
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
-    return t, cfg.roofline_bytes(n_sample)
+    return t, cfg.roofline_bytes(n_sample), len(times)
 
 
 def reference_arm(args, cfg, rank):
@@ -333,11 +334,15 @@ def main():
         del A_h, Y_h
 
     cpu = None
+    if cfg.d * cfg.kappa * cfg.s > (1 << 28):
+        # the oracle builds S explicitly (d·κs nonzeros in float64 CSR): beyond 2^28 nonzeros it does
+        # not fit the host, so no bounded sample of this workload exists for it
+        args.no_cpu_baseline = True
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_s = min(cfg.n, 64)
-        t_cpu, b_cpu = cpu_baseline(cfg, n_s)
+        t_cpu, b_cpu, reps = cpu_baseline(cfg, n_s)
         cpu = {"value": b_cpu / t_cpu / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{n_s} of {cfg.n} columns of {cfg.name}, float64 S build + CSR multiply, median of 2 "
+               "sample": f"{n_s} of {cfg.n} columns of {cfg.name}, float64 S build + CSR multiply, median of {reps} "
                          f"({t_cpu:.2f} s each); numpy/scipy single-threaded",
                "host_cores_available": len(os.sched_getaffinity(0))}
 
@@ -360,7 +365,9 @@ def main():
             "frac_of_8tbs": value / world / 8000.0,
             "ms_min": min(per), "ms_median": statistics.median(per),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic(cfg.name, args.variant) if (args.op == "apply" and args.sketch == "blockperm") else None, "peak_source": peak_src,
+                         "traffic": ncu_traffic(cfg.name + (":t" if args.layout == "t" else "") + (":affine" if args.mode == "affine" else ""),
+                                                args.variant) if (args.op == "apply" and args.sketch == "blockperm") else None,
+                         "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": bytes_rank},
             "gpu_launches": launches,
             "clocks": clk,
