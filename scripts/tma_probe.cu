@@ -31,8 +31,9 @@ __global__ void __launch_bounds__(64, 1) probe(const __grid_constant__ CUtensorM
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full[NST], empty[NST];
-  const int tile = blockIdx.x % ntiles, rr = blockIdx.x / ntiles;
-  const int64_t nk = d / (boxk < 0 ? -boxk : boxk);
+  const bool rowmajor = ntiles == 0;  // rows of d elements (d ≤ boxk), CTAs stream row boxes
+  const int tile = rowmajor ? 0 : blockIdx.x % ntiles, rr = rowmajor ? blockIdx.x : blockIdx.x / ntiles;
+  const int64_t nk = rowmajor ? (int64_t)n / boxr : d / (boxk < 0 ? -boxk : boxk);
   const int64_t k0 = nk * rr / R, k1 = nk * (rr + 1) / R;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) ptx::mbar_init(&full[i], 1), ptx::mbar_init(&empty[i], 1);
@@ -46,7 +47,9 @@ __global__ void __launch_bounds__(64, 1) probe(const __grid_constant__ CUtensorM
     for (int64_t k = k0; k < k1; ++k) {
       ptx::mbar_wait(&empty[s], ph ^ 1);
       ptx::mbar_arrive_expect_tx(&full[s], stage_bytes);
-      if (boxk < 0)  // 3D core-matrix box: (8 elements, boxr vectors, -boxk/8 chunks)
+      if (rowmajor)
+        ptx::tma_load_2d(smem + s * stage_bytes, &tm, &full[s], 0, (int32_t)(k * boxr), pol);
+      else if (boxk < 0)  // 3D core-matrix box: (8 elements, boxr vectors, -boxk/8 chunks)
         tma_load_3d(smem + s * stage_bytes, &tm, &full[s], 0, tile * boxr, (int32_t)(k * (-boxk / 8)), pol);
       else
         ptx::tma_load_2d(smem + s * stage_bytes, &tm, &full[s], (int32_t)(k * boxk), tile * boxr, pol);
@@ -94,9 +97,10 @@ int main(int argc, char** argv) {
     printf("encode failed %d\n", (int)r);
     return 1;
   }
-  const int ntiles = (int)(n / boxr);
-  const int R = ctas / ntiles > 0 ? ctas / ntiles : 1;
-  const int grid = ntiles * R;
+  int ntiles = (int)(n / boxr);
+  int R = ctas / ntiles > 0 ? ctas / ntiles : 1;
+  if (d <= boxk) ntiles = 0, R = ctas;  // row-major mode
+  const int grid = ntiles ? ntiles * R : R;
   const int sb = boxr * (boxk < 0 ? -boxk : boxk) * 2;
   const int smem = NST * sb + 1024;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -136,6 +136,16 @@ def test_bf16_input(variant, layout):
     assert_f32(Yt.T, oracle.apply(osk, Ab), np.linalg.norm(Ab.astype(np.float64), axis=0), "bf16-t tight")
 
 
+@pytest.mark.parametrize("n", [1, 17, 32, 64, 65])
+def test_bf16_narrow(n):
+    """Narrow bf16 inputs take the 64-column tile (n ≤ 64) with the deep ring; 65 the 128 tile."""
+    sk, osk = _pair(64, 16, 2048, 8, 2, seed=11)
+    A = synth.host_matrix("gaussian", sk.d, n, seed=n)
+    Ab = synth.bf16_round(A)
+    Y = _run(sk, A, "tc", dtype=torch.bfloat16)
+    assert_f32(Y, oracle.apply(osk, Ab), np.linalg.norm(Ab.astype(np.float64), axis=0), f"bf16 narrow n={n}")
+
+
 def test_zero_n_and_zero_input():
     sk = Sketch(8, 32, 128, 2, 2, 1)
     A = torch.zeros((sk.d, 0), device="cuda")
@@ -231,6 +241,11 @@ def test_ls_config_transposed_sampled(variant):
 @pytest.mark.parametrize("variant", ["auto"])
 def test_grad_config_sampled(variant):
     _sampled_check(C.GRAD, variant)
+    torch.cuda.empty_cache()
+
+
+def test_smalln_config_sampled():
+    _sampled_check(C.SMALLN, "tc")
     torch.cuda.empty_cache()
 
 
