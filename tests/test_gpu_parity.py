@@ -52,7 +52,9 @@ def _pair(M, Br, Bc, kappa, s, seed=1234, mode="rowpart"):
 @pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("layout", [(8, 32, 128, 2, 2), (16, 64, 128, 4, 2), (128, 32, 8192, 4, 4), (512, 16, 32768, 8, 2),
                                     # band generator paths: C = 1 dense rows (κs = 128), κs = 8 and 12 (batch tails)
-                                    (64, 8, 4096, 16, 8), (32, 64, 2048, 1, 8), (32, 32, 2048, 3, 4)])
+                                    (64, 8, 4096, 16, 8), (32, 64, 2048, 1, 8), (32, 32, 2048, 3, 4),
+                                    # C = 2 and C = 4 whole-piece rows
+                                    (64, 8, 4096, 16, 4), (32, 16, 2048, 8, 4), (16, 16, 1024, 3, 8)])
 def test_selector_columns_bit_exact(variant, layout):
     """A = E_J (unit columns) gives Y = S[:, J]: rows, signs and nnz must match the
     oracle bit-exactly and every value must be exactly ±fp32(1/√(κs))."""
