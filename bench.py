@@ -137,7 +137,7 @@ def cpu_baseline(cfg, n_sample, min_seconds=10.0, max_repeats=8):
     osk = oracle.make_sketch(cfg.M, cfg.B_r, cfg.B_c, cfg.kappa, cfg.s, cfg.seed)
     A = synth.host_matrix("gaussian", cfg.d, n_sample, seed=3, dtype=np.float32)
     times = []
-    while len(times) < 2 or (sum(times) < min_seconds and len(times) < max_repeats):
+    while (len(times) < 2 and sum(times) < 15.0) or (sum(times) < min_seconds and len(times) < max_repeats):
         t0 = time.perf_counter()
         oracle.apply(osk, A)
         times.append(time.perf_counter() - t0)
