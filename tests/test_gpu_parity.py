@@ -148,6 +148,35 @@ def test_bf16_narrow(n):
     assert_f32(Y, oracle.apply(osk, Ab), np.linalg.norm(Ab.astype(np.float64), axis=0), f"bf16 narrow n={n}")
 
 
+@pytest.mark.parametrize("layout", [(32, 32, 2048, 16, 1), (32, 32, 2048, 16, 4), (32, 32, 2048, 16, 8),
+                                    (64, 24, 1024, 16, 8)])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_wide_band_bf16(layout, transposed):
+    """κ·B_r in (256, 512]: four band M-tiles (bf16 only, 64-column tiles). Selector columns must
+    reproduce S bit-exactly; Gaussian data meets the fp32 criterion against the bf16-rounded input."""
+    M, Br, Bc, kappa, s = layout
+    sk, osk = _pair(*layout, seed=21)
+    if (Br // s) & (Br // s - 1):  # C not a power of two: rejected by the tc variant
+        with pytest.raises(BpsError):
+            sk.apply(torch.zeros((sk.d, 8), device="cuda", dtype=torch.bfloat16), variant="tc")
+        return
+    rng = np.random.default_rng(1)
+    J = rng.choice(sk.d, 40, replace=False)
+    E = np.zeros((sk.d, len(J)), dtype=np.float32)
+    E[J, np.arange(len(J))] = 1.0
+    Y = _run(sk, E.T if transposed else E, "tc", dtype=torch.bfloat16, transposed=transposed)
+    Y = Y.T if transposed else Y
+    Sref = oracle.apply(osk, E)
+    np.testing.assert_array_equal(np.sign(Y), np.sign(Sref))
+    nz = Sref != 0
+    assert np.all(np.abs(Y[nz]) == np.float32(1.0 / np.sqrt(kappa * s)))
+    A = synth.host_matrix("gaussian", sk.d, 70, seed=2)
+    Ab = synth.bf16_round(A)
+    Y = _run(sk, A.T if transposed else A, "tc", dtype=torch.bfloat16, transposed=transposed)
+    Y = Y.T if transposed else Y
+    assert_f32(Y, oracle.apply(osk, Ab), np.linalg.norm(Ab.astype(np.float64), axis=0), f"wide {layout} T={transposed}")
+
+
 def test_zero_n_and_zero_input():
     sk = Sketch(8, 32, 128, 2, 2, 1)
     A = torch.zeros((sk.d, 0), device="cuda")
