@@ -65,6 +65,9 @@ typedef enum {
   BPS_VARIANT_SPARSE = 1, /* CUDA-core gather kernel (private smem accumulators, no atomics) */
   BPS_VARIANT_TC = 2      /* tcgen05 tensor-core kernel; BPS_ERR_UNSUPPORTED if the shape is not covered */
 } bps_variant;
+/* tcgen05 coverage (bps_apply / bps_apply_t): B_c % 64 == 0, κ·s ≤ 128, κ·B_r ≤ 256 for fp32 and
+ * ≤ 512 for bf16 (κ·B_r > 256 additionally needs B_r/s a power of two and κ·s % 4 == 0 in the
+ * row-partitioned mode).  Other shapes run on the sparse kernel under BPS_VARIANT_AUTO. */
 
 /*
  * bps_make_sketch — create the sketch S for layout (M, B_r, B_c) and parameters (κ, s, seed).
