@@ -324,12 +324,15 @@ def build_S_csr(sk: Sketch, blocks=None):
 
 def apply(sk: Sketch, A: np.ndarray, blocks=None) -> np.ndarray:
     """Y = S·A in float64 (A: d×n, any float dtype; upcast is exact for fp32/bf16).
-    With `blocks`, returns only those output block rows, stacked."""
+    With `blocks`, returns only those output block rows, stacked.
+
+    Evaluated as the sum over the nonzeros of S only (CSR product; Alg. 1, P:1688-1709 adds
+    σ·a into the s drawn rows of each of the κ output blocks an input row feeds), so the zeros
+    of S never multiply A: with a non-finite a, ±Inf/NaN reach exactly the κ·s rows its
+    column of S names (reading R12) — a dense product would form 0·Inf = NaN everywhere."""
     A64 = np.asarray(A, dtype=np.float64)
     if A64.shape[0] != sk.d:
         raise ValueError("A must have d rows")
-    if blocks is None and sk.k * sk.d <= (1 << 22):
-        return build_S_dense(sk) @ A64
     return build_S_csr(sk, blocks) @ A64
 
 
@@ -346,9 +349,7 @@ def apply_adjoint(sk: Sketch, Yin: np.ndarray) -> np.ndarray:
     Y64 = np.asarray(Yin, dtype=np.float64)
     if Y64.shape[0] != sk.k:
         raise ValueError("Y must have k rows")
-    if sk.k * sk.d <= (1 << 22):
-        return build_S_dense(sk).T @ Y64
-    return build_S_csr(sk).T @ Y64
+    return build_S_csr(sk).T @ Y64  # nonzeros only (R12, as apply)
 
 
 def sketch_rows(sk: Sketch, g: int) -> np.ndarray:

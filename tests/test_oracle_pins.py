@@ -163,6 +163,45 @@ def test_apply_equals_triplet_sum_bruteforce():
     assert np.allclose(oracle.apply(sk, A), Y, rtol=0, atol=1e-13)
 
 
+def test_nonfinite_inputs_follow_the_sparse_sum():
+    """R12: Y = S·A is the sum over the nonzeros of S (Alg. 1); an input element
+    reaches only the κ·s rows its column of S names (κs nonzeros per column).  Pinned
+    against the brute-force triplet loop with Python floats (IEEE: x + Inf = Inf, Inf − Inf = NaN,
+    NaN propagates) and, for a huge finite value, against exact rational arithmetic."""
+    from fractions import Fraction
+
+    sk = oracle.make_sketch(4, 8, 16, 2, 2, seed=3)
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((sk.d, 4))
+    A[5, 0] = np.inf
+    A[9, 1] = np.nan
+    A[17, 2], A[40, 2] = np.inf, -np.inf
+    A[33, 3] = 3.4e38  # beyond the bf16 range, finite in fp32 and fp64
+    Y = oracle.apply(sk, A)
+    ref = [[0.0] * 4 for _ in range(sk.k)]
+    exact3 = [Fraction(0)] * sk.k
+    for g in range(sk.M):
+        for ell, h in enumerate(bp.neighborhood(sk.a, sk.b, sk.M, sk.kappa, g), start=1):
+            for u in range(sk.B_c):
+                for j in range(sk.s):
+                    r, sg = bp.pattern(sk, g, ell, u, j)
+                    for t in range(4):
+                        ref[g * sk.B_r + r][t] += sg * float(A[h * sk.B_c + u, t])
+                    exact3[g * sk.B_r + r] += sg * Fraction(float(A[h * sk.B_c + u, 3]))
+    ref = np.array(ref) / math.sqrt(sk.kappa * sk.s)
+    # non-finite pattern: exactly the rows the brute force puts there
+    assert np.array_equal(np.isnan(Y), np.isnan(ref)) and np.array_equal(np.isposinf(Y), np.isposinf(ref))
+    assert np.array_equal(np.isneginf(Y), np.isneginf(ref))
+    S = oracle.build_S_csr(sk)
+    assert (~np.isfinite(Y[:, 0])).sum() == sk.kappa * sk.s  # one Inf input: κs infinite rows
+    assert set(np.flatnonzero(~np.isfinite(Y[:, 0]))) == set(S[:, 5].nonzero()[0])
+    assert (np.isnan(Y[:, 1])).sum() == sk.kappa * sk.s
+    fin = np.isfinite(ref)
+    assert np.allclose(Y[fin], ref[fin], rtol=1e-12, atol=1e-12)
+    want3 = np.array([float(v) for v in exact3]) / math.sqrt(sk.kappa * sk.s)
+    assert np.all(np.isfinite(Y[:, 3])) and np.allclose(Y[:, 3], want3, rtol=1e-12, atol=1e-9)
+
+
 # --------------------------------------------------------------- identities
 def test_energy_identity():
     """Lemma P:54-65: Σ_g ‖x_N(g)‖² = κ‖x‖² and Σ_g U_Nᵀ U_N = κ UᵀU."""
