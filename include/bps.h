@@ -67,7 +67,9 @@ typedef enum {
 } bps_variant;
 /* tcgen05 coverage (bps_apply / bps_apply_t): B_c % 64 == 0, κ·s ≤ 128, κ·B_r ≤ 256 for fp32 and
  * ≤ 512 for bf16 (κ·B_r > 256 additionally needs B_r/s a power of two and κ·s % 4 == 0 in the
- * row-partitioned mode).  Other shapes run on the sparse kernel under BPS_VARIANT_AUTO. */
+ * row-partitioned mode), d and n < 2^31.  Other shapes run on the sparse kernel under
+ * BPS_VARIANT_AUTO.  The sparse kernel needs B_r ≤ 400 (row-major) / B_r ≤ 192 (transposed) and
+ * ⌈n/128⌉ ≤ 65535; a shape neither kernel covers returns BPS_ERR_UNSUPPORTED. */
 
 /*
  * bps_make_sketch — create the sketch S for layout (M, B_r, B_c) and parameters (κ, s, seed).
@@ -95,14 +97,22 @@ int bps_sketch_info(const bps_sketch* sk, int64_t* d, int64_t* k, uint32_t* a, u
 /*
  * bps_apply — Y = S·A  (output tile Y[gB_r:(g+1)B_r, columns]).
  *   A : device, d×n row-major, element type `dtype`, leading dimension lda ≥ n (elements).
- *   Y : device, k×n row-major fp32, leading dimension ldy ≥ n (elements). Overwritten.
+ *   Y : device, k×n row-major fp32, leading dimension ldy ≥ n (elements). Overwritten; every
+ *       element is written exactly once (no pre-zeroing, no atomics).
  *   bf16 inputs are widened exactly; accumulation is fp32; the scale 1/√(κs) is
  *   applied once at the end as an fp32 constant (R6).
  *   n == 0 is a no-op. A and Y must not overlap.
  *   Alignment: A, Y 16-byte aligned and lda·elem, ldy·4 multiples of 16 bytes,
  *   otherwise BPS_ERR_ALIGNMENT.
- *   Determinism: for a fixed handle, input, n, dtype and variant, Y is bitwise
- *   reproducible run to run.
+ *   Non-finite inputs (R12): an input element reaches only the κ·s rows its column of S
+ *   names (Alg. 1), as in exact arithmetic: ±Inf/NaN appear only there, and
+ *   finite inputs beyond the bf16 range are summed exactly (fp64) rather than overflowing.
+ *   Determinism (R19): for a fixed handle, dtype, layout and variant, each
+ *   element of Y is a fixed function of its input column — bitwise the same run to run, for
+ *   any n, any column split (column shards), any orbit-range split (bps_apply_orbit_range),
+ *   with or without a workspace, on any number of SMs.
+ *   Without a workspace the tc variant uses "halo" ranges (each CTA re-streams κ−1 input
+ *   blocks of halo, ≤ 25 % extra reads, fewer CTAs); bps_apply_ws is the full-occupancy form.
  */
 int bps_apply(const bps_sketch* sk, const void* A, int64_t lda, int64_t n, bps_dtype dtype,
               float* Y, int64_t ldy, void* stream);
@@ -123,14 +133,17 @@ int bps_apply_t_ex(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, 
                    float* Yt, int64_t ldyt, void* stream, int variant);
 
 /*
- * Workspace forms.  With a device workspace of at least bps_workspace_size() bytes the tc
- *   variant splits the input stream into equal stage-granular ranges (one per SM) instead of
- *   whole-block ranges; outputs split between ranges are accumulated into Y and into the
- *   workspace by range parity (each buffer gets ≤ 2 addends per element, so the result is
- *   still bitwise reproducible) and a final pass adds the workspace into Y.  Without a
- *   (large enough) workspace these calls behave like bps_apply / bps_apply_t.
- *   The workspace is caller-owned device memory, 16-byte aligned, not overlapping Y; its
- *   contents are scratch.  bytes = 0 means no workspace is useful for this shape/dtype.
+ * Workspace forms (the full-occupancy tc path; the Python binding always uses them).  With a
+ *   device workspace of at least bps_workspace_size() bytes the tc variant splits the input
+ *   stream into equal group-aligned ranges, one CTA (pair) per SM: the CTA holding an output's
+ *   first accumulation group finishes it, in stream order, from the group partials that the CTAs
+ *   holding its later groups leave in the workspace (epoch-tagged flags, no atomics on Y).  The
+ *   result is bitwise identical to the no-workspace call (see bps_apply).
+ *   Workspace: caller-owned device memory, 256-byte aligned, not overlapping the output; its
+ *   FIRST 256 BYTES MUST BE ZERO before its first use (e.g. cudaMemset once at allocation); each
+ *   call leaves them valid for the next, so no re-zeroing is needed between calls.  One workspace
+ *   must not be used by two calls that may run concurrently.  A too small workspace (or NULL) is
+ *   ignored (no-workspace behaviour).  bytes = 0: the shape has no tc plan (sparse kernel).
  */
 int bps_workspace_size(const bps_sketch* sk, int64_t n, bps_dtype dtype, int transposed, size_t* bytes);
 int bps_apply_ws(const bps_sketch* sk, const void* A, int64_t lda, int64_t n, bps_dtype dtype,
@@ -208,11 +221,19 @@ int bps_orbit(const bps_sketch* sk, int32_t* g_of_pos);
  *            stacked in that order: ((pos_end-pos_begin)+κ-1)·B_c rows × n, row-major, lda.
  *   Y_local: device, the output blocks at orbit positions pos_begin .. pos_end-1,
  *            stacked: (pos_end-pos_begin)·B_r rows × n fp32, row-major, ldy.
- *   Output block at local index i equals rows g_{pos_begin+i}·B_r.. of the full S·A.
+ *   Output block at local index i equals rows g_{pos_begin+i}·B_r.. of the full S·A — bitwise
+ *   (same variant and dtype), so block sharding reproduces the 1-GPU result exactly (R19).
+ * bps_apply_orbit_range_ws / bps_orbit_range_workspace_size: the workspace form (as bps_apply_ws).
  */
 int bps_apply_orbit_range(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end,
                           const void* A_local, int64_t lda, int64_t n, bps_dtype dtype,
                           float* Y_local, int64_t ldy, void* stream, int variant);
+int bps_apply_orbit_range_ws(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end,
+                             const void* A_local, int64_t lda, int64_t n, bps_dtype dtype,
+                             float* Y_local, int64_t ldy, void* workspace, size_t workspace_bytes,
+                             void* stream, int variant);
+int bps_orbit_range_workspace_size(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end, int64_t n,
+                                   bps_dtype dtype, size_t* bytes);
 
 /*
  * bps_pattern_host — host evaluation of the frozen pattern draw (R2-R3), for tests:

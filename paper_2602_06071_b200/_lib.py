@@ -21,7 +21,9 @@ STATUS = {
 }
 EXPORTS = [
     "bps_make_sketch", "bps_free_sketch", "bps_sketch_info", "bps_apply", "bps_apply_t", "bps_apply_ex",
-    "bps_apply_t_ex", "bps_workspace_size", "bps_apply_ws", "bps_apply_t_ws", "bps_orbit", "bps_apply_orbit_range", "bps_pattern_host", "bps_kernel_launches", "bps_version", "bps_last_error",
+    "bps_apply_t_ex", "bps_workspace_size", "bps_apply_ws", "bps_apply_t_ws", "bps_orbit", "bps_apply_orbit_range",
+    "bps_apply_orbit_range_ws", "bps_orbit_range_workspace_size", "bps_pattern_host", "bps_kernel_launches",
+    "bps_version", "bps_last_error",
 ]
 
 
@@ -80,6 +82,12 @@ def _load() -> ctypes.CDLL:
     L.bps_orbit.restype = ctypes.c_int
     L.bps_apply_orbit_range.argtypes = [vp, i64, i64, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_int]
     L.bps_apply_orbit_range.restype = ctypes.c_int
+    if hasattr(L, "bps_apply_orbit_range_ws"):  # absent only in old builds loaded via BPS_LIB for A/B runs
+        L.bps_apply_orbit_range_ws.argtypes = [vp, i64, i64, vp, i64, i64, ctypes.c_int, vp, i64, vp, ctypes.c_size_t,
+                                               vp, ctypes.c_int]
+        L.bps_apply_orbit_range_ws.restype = ctypes.c_int
+        L.bps_orbit_range_workspace_size.argtypes = [vp, i64, i64, i64, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]
+        L.bps_orbit_range_workspace_size.restype = ctypes.c_int
     L.bps_pattern_host.argtypes = [vp, i64, i32, i64, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.bps_pattern_host.restype = ctypes.c_int
     L.bps_kernel_launches.argtypes = []

@@ -124,8 +124,11 @@ static int dispatch(const bps_sketch* sk, const void* in, int64_t ldin, int64_t 
   }
   const bool tc_ok = tc_supported(sk->p, n, dt, transposed, pl) == BPS_OK;
   if (variant == BPS_VARIANT_TC && !tc_ok) return BPS_ERR_UNSUPPORTED;  // message set by tc_supported
-  if (tc_ok && variant != BPS_VARIANT_SPARSE)
-    return launch_tc(sk->p, in, ldin, n, dt, out, ldout, transposed, pl, ws, ws_bytes, st);
+  if (tc_ok && variant != BPS_VARIANT_SPARSE) {
+    const int rc = launch_tc(sk->p, in, ldin, n, dt, out, ldout, transposed, pl, ws, ws_bytes, st);
+    // AUTO: a shape the tc planner cannot launch runs on the sparse kernel (bps.h), nothing was enqueued
+    if (rc != BPS_ERR_UNSUPPORTED || variant == BPS_VARIANT_TC) return rc;
+  }
   return transposed ? launch_sparse_transposed(sk->p, in, ldin, n, dt, out, ldout, pl, st)
                     : launch_sparse_rowmajor(sk->p, in, ldin, n, dt, out, ldout, pl, st);
 }
@@ -364,17 +367,44 @@ int bps_apply_adjoint(const bps_sketch* sk, const float* Y, int64_t ldy, int64_t
   return bps_apply_adjoint_ex(sk, Y, ldy, n, X, ldx, stream, BPS_VARIANT_AUTO);
 }
 
-int bps_apply_orbit_range(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end, const void* A_local, int64_t lda,
-                          int64_t n, bps_dtype dtype, float* Y_local, int64_t ldy, void* stream, int variant) {
+static int check_range(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end) {
   if (!sk) return fail(BPS_ERR_INVALID_ARG, "sketch handle is NULL");
+  if (sk->kind != 0) return fail(BPS_ERR_UNSUPPORTED, "orbit ranges: BlockPerm-SJLT sketches only");
   if (pos_begin < 0 || pos_begin >= sk->M || pos_end <= pos_begin || pos_end > pos_begin + sk->M)
     return fail(BPS_ERR_INVALID_ARG, "need 0 <= pos_begin < M and pos_begin < pos_end <= pos_begin + M");
+  return BPS_OK;
+}
+
+int bps_apply_orbit_range_ws(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end, const void* A_local,
+                             int64_t lda, int64_t n, bps_dtype dtype, float* Y_local, int64_t ldy, void* workspace,
+                             size_t workspace_bytes, void* stream, int variant) {
+  int rc = check_range(sk, pos_begin, pos_end);
+  if (rc) return rc;
   const int64_t L = pos_end - pos_begin;
   const int64_t in_rows = (L + sk->kappa - 1) * sk->B_c;
-  int rc = validate_apply(sk, A_local, lda, in_rows, n, dtype, Y_local, ldy, L * sk->B_r, n, variant);
+  rc = validate_apply(sk, A_local, lda, in_rows, n, dtype, Y_local, ldy, L * sk->B_r, n, variant);
   if (rc || n == 0) return rc;
+  if (workspace && overlaps(workspace, workspace_bytes, Y_local, (size_t)((L * sk->B_r - 1) * ldy + n) * 4))
+    return fail(BPS_ERR_INVALID_ARG, "workspace overlaps the output");
   Placement pl{1, pos_begin, L};
-  return dispatch(sk, A_local, lda, n, dtype, Y_local, ldy, false, pl, stream, variant);
+  return dispatch(sk, A_local, lda, n, dtype, Y_local, ldy, false, pl, stream, variant, workspace, workspace_bytes);
+}
+
+int bps_apply_orbit_range(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end, const void* A_local, int64_t lda,
+                          int64_t n, bps_dtype dtype, float* Y_local, int64_t ldy, void* stream, int variant) {
+  return bps_apply_orbit_range_ws(sk, pos_begin, pos_end, A_local, lda, n, dtype, Y_local, ldy, nullptr, 0, stream,
+                                  variant);
+}
+
+int bps_orbit_range_workspace_size(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end, int64_t n,
+                                   bps_dtype dtype, size_t* bytes) {
+  int rc = check_range(sk, pos_begin, pos_end);
+  if (rc) return rc;
+  if (!bytes) return fail(BPS_ERR_INVALID_ARG, "NULL argument");
+  if (n < 0) return fail(BPS_ERR_INVALID_ARG, "negative n");
+  Placement pl{1, pos_begin, pos_end - pos_begin};
+  *bytes = tc_workspace_bytes(sk->p, n, dtype, false, pl);
+  return BPS_OK;
 }
 
 }  // extern "C"

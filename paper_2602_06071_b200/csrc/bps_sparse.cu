@@ -10,8 +10,10 @@
 //     order at the end, so the result is bitwise reproducible;
 //   * the s hash draws of a row are computed by s lanes at once and broadcast by
 //     shuffles.
-// This is the generic fallback (any B_r ≤ 1280, any n, both layouts); the tcgen05
-// kernel in bps_tc.cu is the fast path.
+// This is the generic fallback (B_r ≤ 400 row-major, B_r ≤ 192 transposed, any n, both
+// layouts); the tcgen05 kernel (bps_tc_kernel.cuh) is the fast path.
+// Non-finite results (R12): fp32 partial sums of finite inputs near FLT_MAX can overflow where
+// the exact sum does not; such elements are recomputed by one thread in fp64 (exact_elem_1t).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -62,6 +64,40 @@ __device__ __forceinline__ float ld1<__nv_bfloat16>(const __nv_bfloat16* p) { re
 __device__ __forceinline__ uint32_t block_g(const SketchParams& p, int range_mode, int64_t pos_begin, uint32_t o) {
   return range_mode ? affine_pow(p, (uint64_t)pos_begin + o, 0u) : o;
 }
+
+// One element of Y by the sparse definition (Alg. 1), fp64, one thread: output o of
+// the launch (full mode: block g = o; range mode: orbit position pos_begin + o), row r, column t.
+template <typename T, bool TRANS>
+__device__ float exact_elem_1t(const SketchParams& p, const T* A, int64_t lda, int range_mode, int64_t pos_begin,
+                               uint32_t o, uint32_t g, uint32_t r, int64_t t) {
+  double acc = 0.0;
+  uint32_t h = g;
+  for (uint32_t ell = 1; ell <= p.kappa; ++ell) {
+    h = affine_step(p, h);
+    const int64_t hrow = (range_mode ? (int64_t)o + ell - 1 : (int64_t)h) * p.B_c;
+    for (uint32_t u = 0; u < p.B_c; ++u) {
+      uint32_t hit = 0, neg = 0;
+      if (p.mode) {
+        const uint64_t z = pattern_hash(p, g, ell, u, 0);
+        for (uint32_t j = 0; j < p.s; ++j) {
+          const Draw d = affine_draw(p, z, j);
+          if (d.row == r) hit = 1, neg = d.neg;
+        }
+      } else {
+        const uint32_t j = r / p.C;
+        const Draw d = draw_from_hash(p, pattern_hash(p, g, ell, u, j), j);
+        hit = d.row == r, neg = d.neg;
+      }
+      if (!hit) continue;
+      const float v = ld1<T>(TRANS ? A + t * lda + hrow + u : A + (hrow + u) * lda + t);
+      acc += neg ? -(double)v : (double)v;
+    }
+  }
+  (void)pos_begin;
+  return (float)(acc * (double)p.scale);
+}
+
+__device__ __forceinline__ bool not_finite(float v) { return (__float_as_uint(v) & 0x7F800000u) == 0x7F800000u; }
 
 constexpr int kRowsPerIter = 4;  // rows u in flight per warp (ILP)
 
@@ -139,7 +175,9 @@ __global__ void __launch_bounds__(256) sparse_rowmajor_kernel(SketchParams p, co
     if (cc >= n) continue;
     float s = 0.f;
     for (int w = 0; w < W; ++w) s += smem[(size_t)w * p.B_r * TN + e];
-    Y[(y_row + r) * ldy + cc] = s * p.scale;
+    float y = s * p.scale;
+    if (not_finite(y)) y = exact_elem_1t<T, false>(p, A, lda, range_mode, pos_begin, o, g, (uint32_t)r, cc);
+    Y[(y_row + r) * ldy + cc] = y;
   }
 }
 
@@ -200,7 +238,9 @@ __global__ void __launch_bounds__(256) sparse_transposed_kernel(SketchParams p, 
     for (uint32_t r = lane; r < p.B_r; r += 32) {
       const float a0 = accs[((size_t)(vgi)*p.B_r + r) * 33 + vl];
       const float a1 = accs[((size_t)(vgi + 4) * p.B_r + r) * 33 + vl];
-      Yt[v * ldyt + y_col + r] = (a0 + a1) * p.scale;
+      float y = (a0 + a1) * p.scale;
+      if (not_finite(y)) y = exact_elem_1t<T, true>(p, X, ldx, range_mode, pos_begin, o, g, r, v);
+      Yt[v * ldyt + y_col + r] = y;
     }
   }
 }

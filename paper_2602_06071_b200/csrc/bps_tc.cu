@@ -1,1476 +1,211 @@
-// bps_tc.cu — tcgen05 tensor-core kernel for Y = S·A (the "tc" variant). DESIGN.md §6.
+// bps_tc.cu — planner and dispatcher of the tcgen05 kernel (the "tc" variant).
+// The kernel itself is bps_tc_kernel.cuh, instantiated in bps_tc_i*.cu (compiled in parallel).
 //
-// Idea: the block sparsity of S is a union of κ permutations that are powers of one
-// affine map f.  Ordering input and output blocks along the orbit
-// g_i = f^i(0) turns the wiring into a sliding window: output i reads input positions
-// i+1..i+κ.  A CTA streams a contiguous range of input positions once (no κ-fold
-// re-read), and for each input block p it builds the dense ±1
-// "band" B_p = [Φ_{g_{p-1},g_p}; …; Φ_{g_{p-κ},g_p}] (κ·B_r × B_c, bf16 exact, rows
-// rotated so output i always lands in slot i mod κ) from the counter hash (R2) and
-// feeds it to tcgen05.mma as the K-major A operand; the data tile (TMA, SW128) is
-// the B operand (MN-major for row-major A, K-major for the transposed layout).
-// D (TMEM, fp32) rows = band rows, columns = data columns.  Accumulation: the tensor
-// core's fp32 accumulate is not round-to-nearest (measured: error grows ∝ #MMAs ×
-// |acc|), so D is fresh for every group of G·64 input rows (two buffers D0/D1
-// alternate) and the epilogue warps fold each group into a TMEM running sum S with
-// IEEE round-to-nearest fp32 adds on the CUDA cores.  The κ slots of S hold the κ
-// outputs in flight; after the last group of input block p the slot of output p−κ is
-// complete: it is scaled by 1/√(κs), stored, and zeroed.
-//   fp32 input: the converter warps split a = hi + lo (two bf16) and the MMA runs
-//   twice (Φ is ±1, exact in bf16) — tf32 would miss the 1e-5 tolerance.
-// Outputs whose κ inputs straddle two CTAs' ranges are combined with red.global.add
-// into a zeroed Y; every such output has exactly two addends, so the result is still
-// bitwise deterministic (a+b == b+a in IEEE arithmetic).
+// The planner picks, from the shape alone: the band M-tiles (κ·B_r ≤ 128/256/512), the column
+// tile BN, the 2-CTA band-sharing cluster, the MMA form (T form for fp32 row-major, K-pair
+// re-layout for bf16 transposed) and the accumulation group G.  G depends on the sketch only
+// (never on n, the device or the decomposition), which is what makes the result canonical:
+// Y is the same bit pattern for every column split, every orbit-range split and every SM count
+// (R19; SURVEY §8(b) determinism contract).
 #include <cuda.h>
-#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <unistd.h>
+
 #include <algorithm>
-#include <cstdio>
+#include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <string>
-#include <type_traits>
-#include <vector>
 
-#include "bps_internal.h"
-#include "bps_ptx.cuh"
+#include "bps_tc.h"
 
 namespace bps {
-namespace {
+namespace tcx {
 
-constexpr int kBK = 64;                   // K rows per pipeline stage (one 128-byte swizzle row of bf16)
-constexpr int kBandTile = 128 * kBK * 2;  // one M-tile (128 band rows) of a band stage, bytes
-constexpr int kMaxGroup = 128;            // K-chunks per accumulation group (precision)
-
-// Warp roles (the issue arbiter favours high warp ids, so the latency-critical single-thread
-// roles take the last two warps): 0-3 epilogue (TMEM lane quarters 0-3) | 4-11 band
-// generator | 12-19 fp32 hi/lo converter (fp32 only) | NWARPS-2 TMA producer |
-// NWARPS-1 MMA issuer (+TMEM alloc).
-template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL = false>
-struct Cfg {
-  // RL ("re-layout", bf16 transposed layout only): TMA loads TWO K-chunks per box without
-  // swizzle (256-byte runs per vector: with vectors megabytes apart, 128-byte runs stream at
-  // ~4.6 TB/s and 256-byte runs at ~7.2 TB/s, scripts/tma_probe.cu), into two consecutive ring
-  // slots; 4 re-layout warps permute the 16-byte pieces in place into the two SW128 K-major
-  // tiles the MMA reads.
-  static_assert(!RL || (!F32 && TRANS && NMT == 1), "RL: bf16 transposed, one band tile");
-  // TF ("transposed form", fp32 row-major only): the data tile is the MMA A operand, written
-  // to TMEM by the converter warps (lane = data column, bf16 pairs along K), and the band is
-  // the K-major smem B operand; D = data columns × band rows.  The converters then never
-  // write shared memory and the MMA reads only the band from it.
-  static_assert(!TF || (F32 && !TRANS && NMT == 1 && BN_ == 128), "TF: fp32 row-major, one band tile");
-  static constexpr int BN = BN_;  // data columns per CTA; TMEM = D (NMT·BN) + S (NMT·BN)
-  static constexpr int ESZ = F32 ? 4 : 2;
-  static constexpr int RAW_STAGE = kBK * BN * ESZ;
-  static constexpr int CONV_HALF = kBK * BN * 2;  // fp32: hi and lo bf16 tiles overwrite the raw stage in place
-  static constexpr int BAND_STAGE = NMT * kBandTile;
-  // CS > 1: the CTAs of a cluster (same input range, CS column tiles) share the band — band
-  // stage t is generated by cluster rank t % CS and bulk-copied to the other CTAs.
-#ifndef BPS_NBAND_CLUSTER
-#define BPS_NBAND_CLUSTER 4
-#endif
-  static constexpr int NBAND_CL = NMT == 1 ? BPS_NBAND_CLUSTER : (NMT == 2 ? 4 : 2);  // NMT = 4: 64 KB stages
-  static constexpr int NBAND = CS > 1 ? (NBAND_CL < CS ? CS : NBAND_CL) : ((NMT == 1 && !F32) ? 3 : 2);
-  static constexpr int LOCALB = NBAND / CS;  // band buffers this CTA generates into
-  static constexpr int BUDGET = 210 * 1024;
-  static constexpr int NRAW_FIT = (BUDGET - NBAND * BAND_STAGE) / RAW_STAGE;
-  // ring depth: 8 stages, 16 for the narrow tile (BN = 64, small n: 8 KB stages, so that enough
-  // bytes are in flight)
-  static constexpr int NRAW_MAX = BN_ <= 64 && !F32 ? 16 : 8;
-  static constexpr int NRAW = (NRAW_FIT > NRAW_MAX ? NRAW_MAX : NRAW_FIT) & (RL ? ~1 : ~0);  // RL: slot pairs
-  static constexpr int OFF_RAW = 0;
-  static constexpr int OFF_BAND = OFF_RAW + NRAW * RAW_STAGE;
-  static constexpr int OFF_CKEY = OFF_BAND + NBAND * BAND_STAGE;  // [2][256] u64 per-block combo keys
-  static constexpr int OFF_CROW = OFF_CKEY + 2 * 256 * 8;  // [128] u32 band-row base σ·B_r + j·C of chunk c
-  static constexpr int OFF_BAR = OFF_CROW + 128 * 4;
-  static constexpr int NCONVA = TF ? 2 : 0;  // TF: TMEM A stages (hi 32 + lo 32 columns each)
-  // raw full/empty, conv full (fp32: per raw stage), band full/empty, acc full, acc free, A full/empty
-  static constexpr int NBARS = 3 * NRAW + 2 * NBAND + 2 + 2 * NCONVA;
-  static constexpr int OFF_TMEMPTR = OFF_BAR + NBARS * 8;
-  static constexpr int SMEM = OFF_TMEMPTR + 16 + 1024;  // + alignment slack
-#ifndef BPS_NBW
-#define BPS_NBW 8
-#endif
-  static constexpr int NBW = BPS_NBW;  // band generator warps (4 .. 4+NBW-1)
-  static_assert(NBW % 4 == 0 && NBW >= 4 && NBW <= 16, "band warps");
-  static constexpr int W_CONV0 = 4 + NBW;  // fp32 converter warps W_CONV0 .. W_CONV0+7
-  static constexpr int NCONVW = F32 ? 8 : (RL ? BN_ / 32 : 0);  // converter (fp32 split / RL re-layout) warps
-  static constexpr int NWARPS = 4 + NBW + NCONVW + 2;
-  static constexpr int NCONVT = NCONVW > 0 ? NCONVW * 32 : 1;  // converter threads
-  static constexpr int W_TMA = NWARPS - 2, W_MMA = NWARPS - 1;
-  static constexpr int NTHREADS = NWARPS * 32;
-  static constexpr int NBANDT = NBW * 32;  // band generator threads
-  static constexpr int NCG = NBANDT / 64;  // combo groups per column u
-  // fp32: the hi and lo tiles are adjacent along N in smem, so ONE MMA with N = 2·BN reads
-  // the band once for both (D columns [0,BN) = band·hi, [BN,2BN) = band·lo).
-  static constexpr int DN = TF ? 128 : (F32 ? 2 * BN : BN);  // D columns per M-tile
-  static constexpr int SN = TF ? 128 : BN;                    // S columns per M-tile
-  static constexpr int OFF_TA = NMT * (DN + SN);              // TF: TMEM A stages start here
-  static constexpr int OFF_D1 = OFF_TA + NCONVA * 64;       // TF: second D tile (lo products)
-  static constexpr int TMEM_NEED = OFF_D1 + (TF ? DN : 0);
-  static constexpr uint32_t TMEM_COLS = (TMEM_NEED <= 256) ? 256 : 512;
-  static constexpr uint32_t IDESC = ptx::idesc_bf16(128, DN, TF ? false : !TRANS);
-  static_assert(NRAW >= 2, "smem: raw ring");
-  static_assert(TMEM_NEED <= 512 && DN <= 256, "TMEM / MMA N");
-  static_assert(BN % 64 == 0 && BN <= 256, "BN");
-  static_assert(SMEM <= 227 * 1024, "smem");
-};
-
-struct TcArgs {
-  SketchParams p;
-  int64_t n;         // columns of A (row-major) or vectors (transposed)
-  float* Y;
-  int64_t ldy;
-  int range_mode;
-  int64_t pos_begin, pos_end;  // owned outputs (range mode)
-  int64_t stream_begin;        // first input position of the launch window
-  int64_t stream_len;          // number of input positions in the window
-  int R;                       // ranges per column tile
-  int nct;                     // column tiles (multiple of the cluster size); CTA = (range, tile)
-  int balanced;                // 1: stage-granular equal ranges, split outputs parity-routed to Y / Y2
-  float* Y2;                   // balanced mode: second accumulation buffer (odd ranges), same shape as Y
-  int64_t ldy2;
-  int G;                       // K-chunks per accumulation group (divides B_c/64)
-  int kgroup;                  // transposed layout: K-chunks whose TMA loads are issued together (≤ NRAW)
-  int tbox;                    // transposed layout, kgroup > 1: vectors per TMA box (divides BN)
-  int nohoist;                 // A/B knob: 1 disables the band generator's register-resident keys
-  uint32_t mma_hint;           // MMA issuer's mbarrier suspend-time hint (ns)
-  int dbg;  // experiment switches (env BPS_TC_DEBUG; 0 in production): 1 no band, 2 no convert, 4 no MMA,
-            // 8 cycle trace, 16 no band proxy fence, 32 band without hashing
-  unsigned long long* trace;   // dbg & 8: per-CTA cycle counters (16 per CTA), else nullptr
-};
-
-// cycle accounting for the BPS_TC_DEBUG=8 trace (compiled in, inactive unless trace != nullptr)
-#ifdef BPS_TC_INSTRUMENT
-struct Tr {
-  unsigned long long* t;
-  __device__ __forceinline__ Tr(unsigned long long* p) : t(p) {}
-  __device__ __forceinline__ unsigned long long now() const { return t ? clock64() : 0ull; }
-  __device__ __forceinline__ void add(int slot, unsigned long long t0) const {
-    if (t) t[slot] += clock64() - t0;
-  }
-};
-#define BPS_DBG(x) (args.dbg & (x))
-#else
-struct Tr {  // production build: instrumentation compiled out
-  __device__ __forceinline__ Tr(unsigned long long*) {}
-  __device__ __forceinline__ unsigned long long now() const { return 0ull; }
-  __device__ __forceinline__ void add(int, unsigned long long) const {}
-};
-#define BPS_DBG(x) 0
-#endif
-
-__device__ __forceinline__ uint32_t mod_pos(int64_t i, uint32_t M) {
-  int64_t r = i % (int64_t)M;
-  return (uint32_t)(r < 0 ? r + M : r);
-}
-
-template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL>
-__global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREADS, 1)
-    bps_tc_kernel(const __grid_constant__ CUtensorMap tmap, const TcArgs args) {
-  using K = Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>;
-  constexpr int BN = K::BN;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + K::OFF_BAR);
-  uint64_t* raw_full = bars;
-  uint64_t* raw_empty = raw_full + K::NRAW;
-  uint64_t* conv_full = raw_empty + K::NRAW;  // fp32: stage converted in place, ready for the MMA
-  uint64_t* band_full = conv_full + K::NRAW;
-  uint64_t* band_empty = band_full + K::NBAND;
-  uint64_t* acc_full = band_empty + K::NBAND;
-  uint64_t* acc_free = acc_full + 1;
-  uint64_t* ta_full = acc_free + 1;        // TF: TMEM A stage written by the converters
-  uint64_t* ta_empty = ta_full + K::NCONVA;  // TF: TMEM A stage consumed by the MMA
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(smem + K::OFF_TMEMPTR);
-  uint64_t* ckey = reinterpret_cast<uint64_t*>(smem + K::OFF_CKEY);
-  uint32_t* crow = reinterpret_cast<uint32_t*>(smem + K::OFF_CROW);
-
-  const SketchParams& p = args.p;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t kappa = p.kappa;
-  const int nk = (int)(p.B_c / kBK);
-  const int G = args.G;
-
-  // ---- this CTA's column tile and input-position range
-  const int ct = blockIdx.x % args.nct, rr = blockIdx.x / args.nct;  // a cluster = CS consecutive tiles
-  const int64_t col0 = (int64_t)ct * BN;
-  // stage s ∈ [S0, S1) of the window = K-chunk s % nk of input position sb + s / nk
-  const int64_t sb = args.stream_begin;
-  int64_t S0, S1;
-  if (args.balanced) {
-    const int64_t Ts = args.stream_len * nk;
-    // RL: whole K-chunk pairs; narrow row-major tile: whole groups of kgroup K-chunks (nk is a
-    // multiple of the unit, so a unit never straddles a block)
-    const int64_t U = RL ? 2 : ((!TRANS && args.kgroup > 1) ? args.kgroup : 1);
-    if (U > 1) {
-      S0 = U * ((Ts / U) * rr / args.R);
-      S1 = U * ((Ts / U) * (rr + 1) / args.R);
-    } else {
-      S0 = Ts * rr / args.R;
-      S1 = Ts * (rr + 1) / args.R;
-    }
-  } else {
-    const int64_t Lq = args.stream_len / args.R, Lrem = args.stream_len % args.R;
-    S0 = (rr * Lq + (rr < Lrem ? rr : Lrem)) * nk;
-    S1 = S0 + (Lq + (rr < Lrem ? 1 : 0)) * nk;
-  }
-  float* const Ysplit = (args.balanced && (rr & 1)) ? args.Y2 : args.Y;  // destination of split outputs
-  const int64_t ldsplit = (args.balanced && (rr & 1)) ? args.ldy2 : args.ldy;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < K::NRAW; ++i) {
-      ptx::mbar_init(&raw_full[i], 1);
-      ptx::mbar_init(&raw_empty[i], TF ? K::NCONVT : 1);  // TF: converters release raw stages
-      ptx::mbar_init(&conv_full[i], K::NCONVT);
-    }
-    for (int i = 0; i < K::NBAND; ++i) {
-      ptx::mbar_init(&band_full[i], CS > 1 ? 1 : K::NBANDT);
-      ptx::mbar_init(&band_empty[i], CS);
-    }
-    ptx::mbar_init(acc_full, 1);
-    ptx::mbar_init(acc_free, 128);
-    for (int i = 0; i < K::NCONVA; ++i) {
-      ptx::mbar_init(&ta_full[i], K::NCONVT);
-      ptx::mbar_init(&ta_empty[i], 1);
-    }
-    ptx::fence_mbar_init();
-    ptx::tma_prefetch(&tmap);
-  }
-  if (warp == K::W_MMA) ptx::tmem_alloc(tmem_ptr, K::TMEM_COLS);
-  ptx::tc_fence_before();
-  if (CS > 1)
-    ptx::cluster_sync();  // peers' barriers are initialised before any remote copy/arrive
-  else
-    __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_ptr;               // D: per-group tensor-core accumulator
-  const uint32_t tmem_S = tmem + NMT * K::DN;    // S: fp32 running sums (RN adds on CUDA cores)
-  const uint32_t tmem_A = tmem + K::OFF_TA;      // TF: A operand stages (data hi | lo)
-
-  if (S1 > S0) {
-    if (warp == K::W_TMA) {
-      // ===================== TMA producer =====================
-      if (lane == 0) {
-        const Tr tr(args.trace ? args.trace + blockIdx.x * 16 : nullptr);
-        const unsigned long long tstart = tr.now();
-        const uint64_t pol = ptx::policy_evict_first();
-        int64_t q = sb + S0 / nk;
-        int kc = (int)(S0 % nk);
-        uint32_t gq = affine_pow(p, (uint64_t)mod_pos(q, p.M), 0u);
-        int s = 0;
-        uint32_t ph = 0;
-        int grp = 0;  // stages of the current K-group still to issue (transposed layout)
-        for (int64_t st = S0; st < S1; ++st) {
-          {
-            const int64_t row0 = args.range_mode ? (q - (args.pos_begin + 1)) * (int64_t)p.B_c : (int64_t)gq * p.B_c;
-            const unsigned long long t0 = tr.now();
-            if (RL) {
-              // one unswizzled box = K-chunks kc, kc+1 of BN vectors (256 B per vector) into ring
-              // slots s, s+1 (contiguous: NRAW is even and pairs start at even slots)
-              if ((kc & 1) == 0) {
-                ptx::mbar_wait_sleep(&raw_empty[s], ph ^ 1, 20);
-                ptx::mbar_wait_sleep(&raw_empty[s + 1], ph ^ 1, 20);
-                tr.add(0, t0);
-                ptx::mbar_arrive_expect_tx(&raw_full[s], 2 * K::RAW_STAGE);
-                ptx::tma_load_2d(smem + K::OFF_RAW + s * K::RAW_STAGE, &tmap, &raw_full[s], (int32_t)(row0 + kc * kBK),
-                                 (int32_t)col0, pol);
-              }
-            } else if (!TRANS && !F32 && BN == 64 && args.kgroup > 1) {
-              // narrow row-major tile (small n): ONE box of 64·kgroup rows fills kgroup consecutive
-              // ring slots (the SW128 MN-major tile of a slot is 64 rows × 128 B, so the slots of a
-              // group are one contiguous 64·kgroup-row tile); the bytes complete on the group's
-              // first slot, which the MMA waits on for every slot of the group
-              if (kc % args.kgroup == 0) {
-                int s2 = s;
-                uint32_t ph2 = ph;
-                for (int i = 0; i < args.kgroup; ++i) {
-                  ptx::mbar_wait_sleep(&raw_empty[s2], ph2 ^ 1, 20);
-                  if (++s2 == K::NRAW) s2 = 0, ph2 ^= 1;
-                }
-                tr.add(0, t0);
-                ptx::mbar_arrive_expect_tx(&raw_full[s], args.kgroup * K::RAW_STAGE);
-                ptx::tma_load_2d(smem + K::OFF_RAW + s * K::RAW_STAGE, &tmap, &raw_full[s], (int32_t)col0,
-                                 (int32_t)(row0 + kc * kBK), pol);
-              }
-            } else if (TRANS && args.kgroup > 1) {
-              // transposed layout: a stage reads kBK·ESZ bytes of each of BN vectors (128 B for
-              // bf16), each vector in another DRAM page.  Issue the K-chunks of an aligned group
-              // together, once ALL their ring slots are free, in sub-boxes of tbox vectors
-              // alternating over the chunks, so the kgroup pieces of a vector (one contiguous
-              // run) reach DRAM a few requests apart and share one row activation.
-              if (grp == 0) {
-                int m = args.kgroup - kc % args.kgroup;
-                if (m > nk - kc) m = nk - kc;
-                if (m > S1 - st) m = (int)(S1 - st);
-                int s2 = s;
-                uint32_t ph2 = ph;
-                for (int i = 0; i < m; ++i) {
-                  ptx::mbar_wait_sleep(&raw_empty[s2], ph2 ^ 1, 20);
-                  ptx::mbar_arrive_expect_tx(&raw_full[s2], K::RAW_STAGE);
-                  if (++s2 == K::NRAW) s2 = 0, ph2 ^= 1;
-                }
-                const int vb = args.tbox;
-                for (int v0 = 0; v0 < BN; v0 += vb) {
-                  int si = s;
-                  for (int i = 0; i < m; ++i) {
-                    uint8_t* dst = smem + K::OFF_RAW + si * K::RAW_STAGE + v0 * (kBK * K::ESZ);
-                    ptx::tma_load_2d(dst, &tmap, &raw_full[si], (int32_t)(row0 + (kc + i) * kBK), (int32_t)(col0 + v0), pol);
-                    if (++si == K::NRAW) si = 0;
-                  }
-                }
-                grp = m;
-              }
-              --grp;
-              tr.add(0, t0);
-            } else {
-              ptx::mbar_wait_sleep(&raw_empty[s], ph ^ 1, 20);
-              tr.add(0, t0);
-              ptx::mbar_arrive_expect_tx(&raw_full[s], K::RAW_STAGE);
-              uint8_t* dst = smem + K::OFF_RAW + s * K::RAW_STAGE;
-              const int32_t r = (int32_t)(row0 + kc * kBK);
-              if (!TRANS) {
-                if (F32) {
-                  ptx::tma_load_2d(dst, &tmap, &raw_full[s], (int32_t)col0, r, pol);
-                } else {
-#pragma unroll
-                  for (int b = 0; b < BN / 64; ++b)
-                    ptx::tma_load_2d(dst + b * (kBK * 128), &tmap, &raw_full[s], (int32_t)(col0 + 64 * b), r, pol);
-                }
-              } else {
-                ptx::tma_load_2d(dst, &tmap, &raw_full[s], r, (int32_t)col0, pol);
-              }
-            }
-            if (++s == K::NRAW) s = 0, ph ^= 1;
-          }
-          if (++kc == nk) kc = 0, ++q, gq = affine_step(p, gq);
-        }
-        tr.add(1, tstart);
-      }
-    } else if (warp == K::W_MMA) {
-      // ===================== MMA issuer =====================
-      // The whole warp runs the loop (descriptors stay warp-uniform, in uniform registers);
-      // one elected lane issues the tcgen05.mma / commit instructions.
-      {
-        const Tr tr((args.trace && lane == 0) ? args.trace + blockIdx.x * 16 : nullptr);
-        const unsigned long long tstart = tr.now();
-        int ds = 0, bs = 0;
-        uint32_t dph = 0, bph = 0, fph = 0;
-        uint64_t* dfull = (F32 || RL) ? conv_full : raw_full;
-        uint64_t* dempty = raw_empty;
-        constexpr int NDS = K::NRAW;
-        const uint32_t data_base = ptx::smem_u32(smem + K::OFF_RAW);
-        constexpr int DSTAGE = K::RAW_STAGE;
-        const uint32_t band_base = ptx::smem_u32(smem + K::OFF_BAND);
-        bool first_group = true;
-        int kc = (int)(S0 % nk);
-        int gi = kc % G;  // position inside the accumulation group (groups restart at block starts)
-        for (int64_t st = S0; st < S1; ++st) {
-          {
-            const bool gstart = st == S0 || gi == 0;
-            const bool gend = st == S1 - 1 || kc == nk - 1 || gi == G - 1;
-            if (gstart && !first_group) {  // D must have been folded into S
-              const unsigned long long t0 = tr.now();
-              ptx::mbar_wait(acc_free, fph);
-              tr.add(2, t0);
-              fph ^= 1;
-              ptx::tc_fence_after();
-            }
-            unsigned long long t0 = tr.now();
-            if (TF)
-              ptx::mbar_wait(&ta_full[(st - S0) & 1], (uint32_t)((st - S0) >> 1) & 1u);
-            else
-              ptx::mbar_wait_hint(&dfull[(!TRANS && args.kgroup > 1) ? (ds & ~(args.kgroup - 1)) : ds], dph, args.mma_hint);
-            tr.add(3, t0);
-            t0 = tr.now();
-            ptx::mbar_wait_hint(&band_full[bs], bph, args.mma_hint);
-            tr.add(4, t0);
-            ptx::tc_fence_after();
-            const uint32_t dbase = data_base + ds * DSTAGE;
-            const uint32_t bbase = band_base + bs * K::BAND_STAGE;
-            if (ptx::elect_one()) {
-            if (TF) {
-              const uint32_t ta = tmem_A + (uint32_t)((st - S0) & 1) * 64;
-#pragma unroll
-              for (int ks = 0; ks < kBK / 16; ++ks) {
-                const uint64_t bdesc = ptx::smem_desc_sw128(bbase + ks * 32, 0, 1024);  // band, K-major
-                if (!BPS_DBG(4)) {
-#ifndef BPS_TF_SHAREDD  // hi and lo accumulate into separate D tiles (independent chains, RN sum in the epilogue)
-                  ptx::mma_bf16_ts(tmem, ta + ks * 8, bdesc, K::IDESC, (gstart && ks == 0) ? 0u : 1u);  // hi
-                  ptx::mma_bf16_ts(tmem + K::OFF_D1, ta + 32 + ks * 8, bdesc, K::IDESC,
-                                   (gstart && ks == 0) ? 0u : 1u);  // lo
-#else
-                  ptx::mma_bf16_ts(tmem, ta + ks * 8, bdesc, K::IDESC, (gstart && ks == 0) ? 0u : 1u);  // hi
-                  ptx::mma_bf16_ts(tmem, ta + 32 + ks * 8, bdesc, K::IDESC, 1u);                          // lo
-#endif
-                }
-              }
-            } else
-#pragma unroll
-            for (int ks = 0; ks < kBK / 16; ++ks) {
-#pragma unroll
-              for (int m = 0; m < NMT; ++m) {
-                const uint64_t adesc = ptx::smem_desc_sw128(bbase + m * kBandTile + ks * 32, 0, 1024);
-                const uint64_t bdesc = TRANS ? ptx::smem_desc_sw128(dbase + ks * 32, 0, 1024)
-                                             : ptx::smem_desc_sw128(dbase + ks * 16 * 128, kBK * 128, 1024);
-                const uint32_t acc = (gstart && ks == 0) ? 0u : 1u;  // fresh per group
-                if (!BPS_DBG(4)) ptx::mma_bf16_ss(tmem + m * K::DN, adesc, bdesc, K::IDESC, acc);
-              }
-            }
-            if (TF)
-              ptx::mma_commit(&ta_empty[(st - S0) & 1]);
-            else
-              ptx::mma_commit(&dempty[ds]);
-            if (CS > 1)
-              ptx::mma_commit_multicast(&band_empty[bs], (uint16_t)((1u << CS) - 1));
-            else
-              ptx::mma_commit(&band_empty[bs]);
-            if (gend) ptx::mma_commit(acc_full);
-            }  // elect_one
-            __syncwarp();
-            if (gend) first_group = false;
-            if (++ds == NDS) ds = 0, dph ^= 1;
-            if (++bs == K::NBAND) bs = 0, bph ^= 1;
-          }
-          if (++kc == nk) kc = 0, gi = 0;
-          else gi = (gi + 1 == G) ? 0 : gi + 1;
-        }
-        tr.add(5, tstart);
-      }
-    } else if (warp < 4) {
-      // ============ epilogue: S += D (fp32 RN) per group; emit the slot that completes ============
-      const int qtr = warp & 3;
-      const uint32_t lane_off = (uint32_t)(qtr * 32) << 16;
-      {  // S = 0
-        uint32_t z[16];
-#pragma unroll
-        for (int t = 0; t < 16; ++t) z[t] = 0u;
-        for (int c = 0; c < NMT * K::SN; c += 16) ptx::tmem_st16(tmem_S + lane_off + c, z);
-        ptx::tmem_wait_st();
-      }
-      auto emit = [&](int64_t i, uint32_t rho, const float* vals, int c0) {
-        // vals: 16 sums of band row rho (slot of output i), columns col0+c0 .. +15
-        const bool owned = args.range_mode ? (i >= args.pos_begin && i < args.pos_end) : true;
-        if (!owned) return;
-        const uint32_t lo = mod_pos(i, kappa) * p.B_r;
-        // complete iff every stage of input blocks i+1 .. i+κ lies in this CTA's range
-        const bool complete = (i + 1 - sb) * nk >= S0 && (i + (int64_t)kappa + 1 - sb) * nk <= S1;
-        const int64_t row = (args.range_mode ? (i - args.pos_begin) * (int64_t)p.B_r
-                                             : (int64_t)affine_pow(p, (uint64_t)mod_pos(i, p.M), 0u) * p.B_r) +
-                            (int64_t)(rho - lo);
-        const int64_t cbase = col0 + c0;
-        float* const Yd = complete ? args.Y : Ysplit;
-        const int64_t ldd = complete ? args.ldy : ldsplit;
-        if (!TRANS) {
-          float* y = Yd + row * ldd + cbase;
-#pragma unroll
-          for (int t = 0; t < 16; t += 4) {
-            const float a0 = vals[t] * p.scale, a1 = vals[t + 1] * p.scale;
-            const float a2 = vals[t + 2] * p.scale, a3 = vals[t + 3] * p.scale;
-            if (cbase + t + 3 < args.n) {
-              if (complete) *reinterpret_cast<float4*>(y + t) = make_float4(a0, a1, a2, a3);
-              else ptx::red_add_v4(y + t, a0, a1, a2, a3);
-            } else {
-              const float a[4] = {a0, a1, a2, a3};
-              for (int e = 0; e < 4; ++e)
-                if (cbase + t + e < args.n) {
-                  if (complete) y[t + e] = a[e];
-                  else ptx::red_add(y + t + e, a[e]);
-                }
-            }
-          }
-        } else {
-#pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            if (cbase + t < args.n) {
-              float* y = Yd + (cbase + t) * ldd + row;
-              const float a = vals[t] * p.scale;
-              if (complete) *y = a;
-              else ptx::red_add(y, a);
-            }
-          }
-        }
-      };
-      // TF: lanes are data columns, TMEM columns are band rows; emit the band rows [lo, hi) of
-      // chunk c0 (16 TMEM columns) for output i: row (out_row0 + ρ − lo), column col0 + lane
-      auto emitT = [&](int64_t i, const float* vals, int c0) {
-        const bool owned = args.range_mode ? (i >= args.pos_begin && i < args.pos_end) : true;
-        if (!owned) return;
-        const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
-        const bool complete = (i + 1 - sb) * nk >= S0 && (i + (int64_t)kappa + 1 - sb) * nk <= S1;
-        const int64_t row0 = args.range_mode ? (i - args.pos_begin) * (int64_t)p.B_r
-                                             : (int64_t)affine_pow(p, (uint64_t)mod_pos(i, p.M), 0u) * p.B_r;
-        const int64_t col = col0 + qtr * 32 + lane;
-        if (col >= args.n) return;
-        float* const Yd = complete ? args.Y : Ysplit;
-        const int64_t ldd = complete ? args.ldy : ldsplit;
-#pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          const uint32_t rho = (uint32_t)c0 + t;
-          if (rho < lo || rho >= hi) continue;
-          float* y = Yd + (row0 + (int64_t)(rho - lo)) * ldd + col;
-          const float a = vals[t] * p.scale;
-          if (complete) *y = a;
-          else ptx::red_add(y, a);
-        }
-      };
-      uint32_t aph = 0;
-      const Tr tr((args.trace && threadIdx.x == 0) ? args.trace + blockIdx.x * 16 : nullptr);
-      const unsigned long long tstart = tr.now();
-      int kc = (int)(S0 % nk);
-      int gi = kc % G;
-      int64_t q = sb + S0 / nk;
-      for (int64_t st = S0; st < S1;
-           ++st, q += (kc + 1 == nk), gi = (kc + 1 == nk || gi + 1 == G) ? 0 : gi + 1, kc = (kc + 1 == nk) ? 0 : kc + 1) {
-        const bool gend = st == S1 - 1 || kc == nk - 1 || gi == G - 1;
-        if (!gend) continue;
-        const int64_t i = q - (int64_t)kappa;  // output completed by input block q (if q ends here)
-        const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
-        {
-          const unsigned long long t0 = tr.now();
-          ptx::mbar_wait_sleep(acc_full, aph, 32);
-          tr.add(9, t0);
-          aph ^= 1;
-          ptx::tc_fence_after();
-          const bool last = kc == nk - 1;  // input block q fully streamed: output q-κ is done here
-          if (TF) {
-#pragma unroll 1
-            for (int c0 = 0; c0 < K::SN; c0 += 16) {
-              uint32_t d[16], sv[16];
-              ptx::tmem_ld16(tmem + lane_off + c0, d);
-              ptx::tmem_ld16(tmem_S + lane_off + c0, sv);
-              float tot[16];
-#ifndef BPS_TF_SHAREDD
-              uint32_t d1[16];
-              ptx::tmem_ld16(tmem + K::OFF_D1 + lane_off + c0, d1);
-              ptx::tmem_wait_ld();
-#pragma unroll
-              for (int t = 0; t < 16; ++t)
-                tot[t] = __uint_as_float(sv[t]) + (__uint_as_float(d[t]) + __uint_as_float(d1[t]));
-#else
-              ptx::tmem_wait_ld();
-#pragma unroll
-              for (int t = 0; t < 16; ++t) tot[t] = __uint_as_float(sv[t]) + __uint_as_float(d[t]);
-#endif
-              const bool hit = last && (uint32_t)c0 < hi && (uint32_t)c0 + 16 > lo;  // warp-uniform
-              if (hit) emitT(i, tot, c0);
-#pragma unroll
-              for (int t = 0; t < 16; ++t)
-                sv[t] = (hit && (uint32_t)c0 + t >= lo && (uint32_t)c0 + t < hi) ? 0u : __float_as_uint(tot[t]);
-              ptx::tmem_st16(tmem_S + lane_off + c0, sv);
-            }
-          } else
-#pragma unroll 1
-          for (int m = 0; m < NMT; ++m) {
-            const uint32_t rho = m * 128 + qtr * 32 + lane;
-            const bool in_slot = last && rho >= lo && rho < hi;
-#pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-              uint32_t d[16], sv[16];
-              ptx::tmem_ld16(tmem + lane_off + m * K::DN + c0, d);
-              ptx::tmem_ld16(tmem_S + lane_off + m * BN + c0, sv);
-              float tot[16];
-              if (F32) {  // hi and lo partial products
-                uint32_t dl[16];
-                ptx::tmem_ld16(tmem + lane_off + m * K::DN + BN + c0, dl);
-                ptx::tmem_wait_ld();
-#pragma unroll
-                for (int t = 0; t < 16; ++t)
-                  tot[t] = __uint_as_float(sv[t]) + (__uint_as_float(d[t]) + __uint_as_float(dl[t]));
-              } else {
-                ptx::tmem_wait_ld();
-#pragma unroll
-                for (int t = 0; t < 16; ++t) tot[t] = __uint_as_float(sv[t]) + __uint_as_float(d[t]);
-              }
-              if (in_slot) emit(i, rho, tot, c0);
-#pragma unroll
-              for (int t = 0; t < 16; ++t) sv[t] = in_slot ? 0u : __float_as_uint(tot[t]);
-              ptx::tmem_st16(tmem_S + lane_off + m * BN + c0, sv);
-            }
-          }
-          ptx::tmem_wait_st();
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(acc_free);
-        }
-      }
-      tr.add(10, tstart);
-      // range end: outputs fed by the last input block that are still open hold partial sums in S
-      const int64_t q_last = sb + (S1 - 1) / nk;
-      const bool full_end = (S1 - 1) % nk == nk - 1;
-      for (int64_t i = q_last - (int64_t)kappa + (full_end ? 1 : 0); i <= q_last - 1; ++i) {
-        const uint32_t lo = mod_pos(i, kappa) * p.B_r, hi = lo + p.B_r;
-        if (TF) {
-          for (int c0 = (int)(lo & ~15u); c0 < (int)hi; c0 += 16) {
-            uint32_t sv[16];
-            ptx::tmem_ld16(tmem_S + lane_off + c0, sv);
-            ptx::tmem_wait_ld();
-            float tot[16];
-#pragma unroll
-            for (int t = 0; t < 16; ++t) tot[t] = __uint_as_float(sv[t]);
-            emitT(i, tot, c0);
-          }
-          continue;
-        }
-#pragma unroll 1
-        for (int m = 0; m < NMT; ++m) {
-          const uint32_t base = m * 128 + qtr * 32;
-          if (base + 32 <= lo || base >= hi) continue;  // warp-uniform
-          const uint32_t rho = base + lane;
-          const bool in_slot = rho >= lo && rho < hi;
-#pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t sv[16];
-            ptx::tmem_ld16(tmem_S + lane_off + m * BN + c0, sv);
-            ptx::tmem_wait_ld();
-            float tot[16];
-#pragma unroll
-            for (int t = 0; t < 16; ++t) tot[t] = __uint_as_float(sv[t]);
-            if (in_slot) emit(i, rho, tot, c0);
-          }
-        }
-      }
-    } else if (warp >= 4 && warp < 4 + K::NBW) {
-      // the intra-block mode is a launch constant: specialise the whole generator on it
-      auto band_gen = [&](auto affine_tag, auto fast_tag) {
-        constexpr bool AFF = decltype(affine_tag)::value;
-        // FAST (row-partitioned only): C = B_r/s a power of two and κs a multiple of 4·NCG, so every
-        // thread owns a whole number of 4-chunk batches (no tail predication, immediate table
-        // offsets), the row offset is a shift, and the stale entries are kept as 16-bit entry
-        // offsets (clearing = one extract + one store).  C = 1 (s = B_r) writes every band row of
-        // every column each stage, so nothing needs clearing at all.
-        constexpr bool FAST = decltype(fast_tag)::value >= 1;
-        constexpr bool FULL = decltype(fast_tag)::value >= 2;  // κs a multiple of 4·NCG: no batch tail
-        // HOIST (κs = 4·NCG: exactly one batch of 4 chunks per thread): the thread's 4 keys and
-        // row bases live in registers, reloaded once per input block instead of every stage
-        constexpr bool HOIST = decltype(fast_tag)::value == 6;
-        uint64_t hk[4] = {0, 0, 0, 0};
-        uint32_t hc[4] = {0, 0, 0, 0};
-        // DENSE (C = B_r/s ∈ {1, 2, 4}): whole 16-byte pieces, CP = C rows per chunk
-        constexpr bool DENSE = decltype(fast_tag)::value >= 3 && decltype(fast_tag)::value <= 5;
-        constexpr int CP = DENSE ? (1 << (decltype(fast_tag)::value - 3)) : 1;
-        constexpr int NPW = FAST ? 8 : 4;  // prev words per buffer
-        // ===================== band generator =====================
-        // Thread (u, cg) writes column u of every band stage for the row chunks c = cg + NCG·t,
-        // c = σ·s + j (slot σ, chunk j).  A chunk's rows [σB_r + jC, +C) are owned by one thread
-        // per column, so each thread can clear the single entry it wrote into this buffer
-        // NBAND stages ago and write the new one without any barrier (no zero-fill pass).
-        const int bt = threadIdx.x - 128;
-        const uint32_t u = (uint32_t)bt & (kBK - 1);
-        const uint32_t cg = (uint32_t)bt >> 6;  // 0..NCG-1
-        const uint32_t ncombo = kappa * p.s;
-        const uint32_t T = ncombo > cg ? (ncombo - cg + K::NCG - 1) / K::NCG : 0;  // chunks of this thread (≤ 32)
-        const bool zf = ncombo > 16u * K::NCG;  // stale rows no longer fit the prev registers (4 words)
-        const uint32_t band_u32 = ptx::smem_u32(smem + K::OFF_BAND);
-        const uint32_t ucol = u >> 3, ulo = (u & 7) * 2;
-        auto entry = [&](uint32_t sbase, uint32_t rho) {
-          // row ρ of the stage at ρ·128 (M-tiles of 128 rows are contiguous: kBandTile = 128·128),
-          // SW128: 16-byte chunk index XOR (ρ mod 8)
-          static_assert(kBandTile == 128 * 128, "band tile layout");
-          return sbase + rho * 128 + (((rho ^ ucol) & 7) << 4) + ulo;
-        };
-        {  // band buffers start zeroed; chunk row bases (fixed for the whole launch)
-          uint4* bz = reinterpret_cast<uint4*>(smem + K::OFF_BAND);
-          for (int i = bt; i < K::NBAND * K::BAND_STAGE / 16; i += K::NBANDT) bz[i] = make_uint4(0, 0, 0, 0);
-          for (uint32_t c = bt; c < ncombo; c += K::NBANDT) crow[c] = band_crow(p, c / p.s, c % p.s);
-        }
-        // rows written LOCALB local stages ago: 4 rows per word (κ·B_r ≤ 256), or (FAST) 2 entry
-        // offsets per word
-        uint32_t prev[K::LOCALB][NPW];
-        const uint32_t crank = CS > 1 ? ptx::cluster_ctarank() : 0u;
-        int64_t local_no = 0;
-  #pragma unroll
-        for (int b = 0; b < K::LOCALB; ++b)
-  #pragma unroll
-          for (int w = 0; w < NPW; ++w) prev[b][w] = 0;
-        const uint32_t cshift = 32u - (31u - (uint32_t)__clz(p.C));  // FAST: off = z_hi >> (32 - log2 C)
-        if constexpr (FAST) {
-          // before the first write of a buffer, "clear" the first entry of the thread's own chunk
-          // (zero in a fresh buffer, and rewritten or left zero by the write that follows)
-  #pragma unroll
-          for (int w = 0; w < NPW; ++w) {
-            uint32_t v = 0;
-  #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const uint32_t c = cg + K::NCG * (2 * w + h);
-              const uint32_t r = c < ncombo ? band_crow(p, c / p.s, c % p.s) : 0u;
-              v |= (r * 128u + (((r ^ ucol) & 7u) << 4)) << (16 * h);
-            }
-  #pragma unroll
-            for (int b = 0; b < K::LOCALB; ++b) prev[b][w] = v;
-          }
-        }
-        int bs = 0;
-        uint32_t bph = 0;
-        int64_t stage_no = 0;
-        const Tr tr((args.trace && bt == 0) ? args.trace + blockIdx.x * 16 : nullptr);
-        const unsigned long long tstart = tr.now();
-        int kc = (int)(S0 % nk);
-        int64_t q = sb + S0 / nk;
-        for (int64_t st = S0; st < S1; ++st, q += (kc + 1 == nk), kc = (kc + 1 == nk) ? 0 : kc + 1, ++stage_no) {
-          const int par = (int)(q & 1);  // tables double-buffered by block parity
-          uint64_t* ck = ckey + par * 256;
-          {
-            const bool local = CS == 1 || (uint32_t)bs % CS == crank;
-            unsigned long long t0 = tr.now();
-            if (local || bt == 0) ptx::mbar_wait_sleep(&band_empty[bs], bph ^ 1, 20);
-            tr.add(6, t0);
-            t0 = tr.now();
-            if (kc == 0 || st == S0) {
-              // per input block q: hash key of chunk (σ, j): the output i ≡ σ (mod κ) fed by q is
-              // i = q - ℓ with ℓ = ((q - σ - 1) mod κ) + 1
-              for (uint32_t c = bt; c < ncombo; c += K::NBANDT) {
-                const uint32_t sig = c / p.s, j = c % p.s;
-                const uint32_t ell = mod_pos(q - (int64_t)sig - 1, kappa) + 1;
-                const uint32_t g = affine_pow(p, (uint64_t)mod_pos(q - (int64_t)ell, p.M), 0u);
-                const uint64_t key = (((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | (uint64_t)band_jfield(p, j)) ^ p.K;
-                if constexpr (AFF) {
-                  ck[c] = key;
-                } else {  // row-partitioned: store the folded key (L1 | P1 << 32), see mix64_folded
-                  uint32_t L1, P1;
-                  mix64_fold_key(key, L1, P1);
-                  ck[c] = ((uint64_t)P1 << 32) | L1;
-                }
-              }
-              ptx::named_bar_sync(1, K::NBANDT);
-              if constexpr (HOIST) {
-  #pragma unroll
-                for (int i = 0; i < 4; ++i) hk[i] = ck[cg + K::NCG * i], hc[i] = crow[cg + K::NCG * i];
-              }
-              tr.add(7, t0);
-            }
-            const uint64_t uk = (uint64_t)((uint32_t)kc * kBK + u) << 8;
-            const uint32_t sbase = band_u32 + bs * K::BAND_STAGE;
-            if (!local) {  // band stage generated by cluster peer `bs`: expect its bulk copy
-              if (bt == 0) ptx::mbar_arrive_expect_tx(&band_full[bs], K::BAND_STAGE);
-              if (++bs == K::NBAND) bs = 0, bph ^= 1;
-              continue;
-            }
-            bool clear = local_no >= K::LOCALB;
-            ++local_no;
-            const bool zero_fill = AFF ? kappa > 4u * K::NCG : (DENSE ? false : (zf && p.C > 1u));
-            if (zero_fill && clear) {
-              // more stale entries per thread than the 4 prev words hold: zero-fill the stage
-              // cooperatively, then write (one barrier per stage)
-              uint4* bz = reinterpret_cast<uint4*>(smem + K::OFF_BAND + bs * K::BAND_STAGE);
-              for (int i = bt; i < K::BAND_STAGE / 16; i += K::NBANDT) bz[i] = make_uint4(0, 0, 0, 0);
-              ptx::named_bar_sync(4, K::NBANDT);
-            }
-            if (zero_fill) clear = false;
-            uint32_t nw[NPW];
-  #pragma unroll
-            for (int w = 0; w < NPW; ++w) nw[w] = 0;
-            if constexpr (DENSE) {
-              // C = B_r/s ∈ {1, 2, 4}: chunk c owns the CP band rows crow[c] .. +CP-1 and has exactly
-              // one ±1 per column among them, so every row of the chunk is rewritten each stage as
-              // whole 16-byte SW128 pieces (8 columns): per item (chunk, 8-column group) 8
-              // independent hashes (ILP 8), CP vector stores, no per-entry addressing and nothing
-              // to clear (rows ≥ κB_r stay zero from the initial fill).
-              const uint32_t xk = (uint32_t)kc * (uint32_t)kBK;
-              for (uint32_t q = (uint32_t)bt; q < ncombo * 8u; q += K::NBANDT) {
-                const uint32_t c = q >> 3, ch = q & 7u;
-                const uint64_t k = ck[c];
-                const uint32_t r0 = crow[c];
-                const uint32_t x0 = (xk + ch * 8u) << 8;
-                uint32_t v[8], ro[8];
-  #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  uint32_t h, l;
-                  mix64_folded((uint32_t)k, (uint32_t)(k >> 32), x0 + ((uint32_t)e << 8), h, l);
-                  v[e] = (0x3F80u | (l << 15)) & 0xFFFFu;  // ±1.0, sign = z & 1
-                  ro[e] = CP == 1 ? 0u : (h >> (32 - (CP == 2 ? 1 : 2)));  // R3: (z_hi · C) >> 32
-                }
-  #pragma unroll
-                for (int rr = 0; rr < CP; ++rr) {
-                  uint32_t w[4];
-  #pragma unroll
-                  for (int j = 0; j < 4; ++j)
-                    w[j] = (ro[2 * j] == (uint32_t)rr ? v[2 * j] : 0u) | ((ro[2 * j + 1] == (uint32_t)rr ? v[2 * j + 1] : 0u) << 16);
-                  const uint32_t rho = r0 + (uint32_t)rr;
-                  const uint32_t addr = sbase + rho * 128u + (((ch ^ rho) & 7u) << 4);
-                  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]), "r"(w[1]), "r"(w[2]),
-                               "r"(w[3])
-                               : "memory");
-                }
-              }
-            } else if constexpr (FAST) {
-              const uint32_t x = (uint32_t)uk;  // counter low word: (kc·64 + u) << 8
-              const uint32_t ebase = sbase + ulo;
-              const bool do_clear = !zero_fill && p.C > 1u;
-              const bool full = FULL;
-              const uint64_t* ckt = ck + cg;
-              const uint32_t* crt = crow + cg;
-  #pragma unroll
-              for (int w = 0; w < 8; ++w) {
-                if ((uint32_t)w * 4 >= T) break;
-                uint32_t hi[4], lo[4], cr[4];
-  #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const uint64_t k = HOIST ? hk[i] : ckt[K::NCG * (4 * w + i)];
-                  cr[i] = HOIST ? hc[i] : crt[K::NCG * (4 * w + i)];
-                  mix64_folded((uint32_t)k, (uint32_t)(k >> 32), x, hi[i], lo[i]);
-                }
-  #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const bool on = full || (uint32_t)(4 * w + i) < T;  // κs/NCG not a multiple of 4: tail
-                  const uint32_t rho = cr[i] + ptx::shr_clamp(hi[i], cshift);  // R3 for C = 2^m
-                  const uint32_t off = rho * 128u + (((rho ^ ucol) & 7u) << 4);
-                  if (w < 4 && on) {
-                    if (do_clear) ptx::st_shared_u16(ebase + ((prev[0][2 * w + (i >> 1)] >> (16 * (i & 1))) & 0xFFFFu), 0);
-                    nw[2 * w + (i >> 1)] |= off << (16 * (i & 1));
-                  }
-                  if (on) ptx::st_shared_u16(ebase + off, (uint16_t)(0x3F80u | (lo[i] << 15)));  // ±1.0, sign = z & 1
-                }
-              }
-            } else if constexpr (AFF) {
-              // AffineUnique (R18), slot-major: thread (u, cg) owns the whole column u of slots
-              // σ ≡ cg (mod NCG): ONE hash per (σ, u) gives α, β and the s signs; the s rows
-              // (α·j + β) mod B_r are walked incrementally.  Clearing re-walks last use's (α, β)
-              // (kept as α | β<<16 in prev) — same thread, so no barrier.
-  #pragma unroll
-              for (int t = 0; t < 16; ++t) {
-                const uint32_t sig = cg + K::NCG * t;
-                if (sig >= kappa) break;
-                const uint32_t base = sig * p.B_r;
-                if (t < 4 && clear) {
-                  const uint32_t w = prev[0][t & 3], a0 = w & 0xFFFFu;
-                  uint32_t r = w >> 16;
-                  for (uint32_t j = 0; j < p.s; ++j, r = (r + a0) & p.Brmask)
-                    ptx::st_shared_u16(entry(sbase, base + r), 0);
-                }
-                const uint64_t z = mix64(ck[sig * p.s] ^ uk);
-                const uint32_t alpha = (uint32_t)(((((z >> 32) & 0xFFFFu) * p.B_r) >> 16) | 1u);
-                const uint32_t beta = (uint32_t)(((z >> 48) * p.B_r) >> 16);
-                uint32_t r = beta, zs = (uint32_t)z;
-                for (uint32_t j = 0; j < p.s; ++j, r = (r + alpha) & p.Brmask, zs >>= 1)
-                  ptx::st_shared_u16(entry(sbase, base + r), (zs & 1u) ? (uint16_t)0xBF80 : (uint16_t)0x3F80);
-                if (t < 4) nw[t & 3] = alpha | (beta << 16);
-              }
-            } else if (!BPS_DBG(1)) {
-              // row-partitioned (R1-R3): one hash per (chunk, u).  The 4 chunks of a batch are
-              // independent (disjoint row ranges), so the tail of the batch is predicated rather
-              // than branched and the compiler interleaves the four hash/store chains.
-              const uint32_t x = (uint32_t)uk;  // counter low word: (kc·64 + u) << 8
-  #pragma unroll
-              for (int w = 0; w < 8; ++w) {
-                if ((uint32_t)w * 4 >= T) break;
-                uint32_t hi[4], lo[4], cr[4];
-  #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  uint32_t c = cg + K::NCG * (4 * w + i);
-                  c = c < ncombo ? c : cg;
-                  const uint64_t k = ck[c];
-                  cr[i] = crow[c];
-                  if (BPS_DBG(32)) {
-                    hi[i] = (uint32_t)k ^ x;
-                    lo[i] = (uint32_t)(k >> 32);
-                  } else {
-                    mix64_folded((uint32_t)k, (uint32_t)(k >> 32), x, hi[i], lo[i]);
-                  }
-                }
-  #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const bool on = (uint32_t)(4 * w + i) < T;
-                  if (w < 4 && clear && on) ptx::st_shared_u16(entry(sbase, (prev[0][w & 3] >> (8 * i)) & 0xFFu), 0);
-                  const uint32_t rho = cr[i] + __umulhi(hi[i], p.C);  // R3
-                  const uint32_t val = 0x3F80u | ((lo[i] & 1u) << 15);  // ±1.0 bf16, sign = z & 1
-                  if (on) ptx::st_shared_u16(entry(sbase, rho), (uint16_t)val);
-                  if (w < 4 && on) nw[w & 3] |= rho << (8 * i);
-                }
-              }
-            }
-  #pragma unroll
-            for (int b = 0; b + 1 < K::LOCALB; ++b)
-  #pragma unroll
-              for (int w = 0; w < NPW; ++w) prev[b][w] = prev[b + 1][w];
-  #pragma unroll
-            for (int w = 0; w < NPW; ++w) prev[K::LOCALB - 1][w] = nw[w];
-            if (!BPS_DBG(16)) ptx::fence_proxy_async_smem();
-            if (CS > 1) {
-              ptx::named_bar_sync(3, K::NBANDT);  // whole stage written (and fenced) by all band threads
-              if (bt == 0) {
-                const uint32_t src = band_u32 + bs * K::BAND_STAGE;
-                const uint32_t bar = ptx::smem_u32(&band_full[bs]);
-                for (uint32_t r = 1; r < (uint32_t)CS; ++r) {
-                  const uint32_t peer = (crank + r) % CS;
-                  ptx::bulk_copy_to_peer(ptx::mapa(src, peer), src, K::BAND_STAGE, ptx::mapa(bar, peer));
-                }
-                ptx::mbar_arrive(&band_full[bs]);
-              }
-            } else {
-              ptx::mbar_arrive(&band_full[bs]);
-            }
-            if (++bs == K::NBAND) bs = 0, bph ^= 1;
-          }
-        }
-        tr.add(8, tstart);
-      };
-      const uint32_t ncomb = kappa * p.s;
-      if (p.mode)
-        band_gen(std::true_type{}, std::integral_constant<int, 0>{});
-      else if (p.C == 1u)
-        band_gen(std::false_type{}, std::integral_constant<int, 3>{});
-      else if (p.C == 2u)
-        band_gen(std::false_type{}, std::integral_constant<int, 4>{});
-      else if (p.C == 4u)
-        band_gen(std::false_type{}, std::integral_constant<int, 5>{});
-      else if ((p.C & (p.C - 1u)) == 0u && ncomb == 4u * K::NCG && !args.nohoist)
-        band_gen(std::false_type{}, std::integral_constant<int, 6>{});
-      else if ((p.C & (p.C - 1u)) == 0u && ncomb % (4u * K::NCG) == 0u)
-        band_gen(std::false_type{}, std::integral_constant<int, 2>{});
-      else if ((p.C & (p.C - 1u)) == 0u && ncomb % K::NCG == 0u)
-        band_gen(std::false_type{}, std::integral_constant<int, 1>{});
-      else
-        band_gen(std::false_type{}, std::integral_constant<int, 0>{});
-    } else if (TF && warp >= K::W_CONV0 && warp < K::W_CONV0 + 8) {
-      // ============ TF converter: fp32 column -> TMEM A operand (hi | lo bf16 pairs) ============
-      // warp w: TMEM lane quarter w % 4 (data columns 32q..32q+31), K rows 32h..32h+31 (h = (w-12)/4).
-      // A stage layout: lane = data column, 32-bit column j holds K rows (2j, 2j+1) (low half = even
-      // row); hi at +0..31, lo at +32..63.  The raw stage is released as soon as it is in registers.
-      const int cv = threadIdx.x - K::W_CONV0 * 32;
-      const int qtr = warp & 3, h = (warp - K::W_CONV0) >> 2;
-      const uint32_t lane_off = (uint32_t)(qtr * 32) << 16;
-      const int col = qtr * 32 + lane;
-      int rs = 0;
-      uint32_t rph = 0;
-      const int64_t total = S1 - S0;
-      for (int64_t it = 0; it < total; ++it) {
-        ptx::mbar_wait(&raw_full[rs], rph);
-        const float* raw = reinterpret_cast<const float*>(smem + K::OFF_RAW + rs * K::RAW_STAGE) + (h * 32) * BN + col;
-        float a[32];
-#pragma unroll
-        for (int r = 0; r < 32; ++r) a[r] = raw[r * BN];
-        ptx::mbar_arrive(&raw_empty[rs]);  // values are in registers
-        if (++rs == K::NRAW) rs = 0, rph ^= 1;
-        const uint32_t ab = (uint32_t)(it & 1);
-        ptx::mbar_wait(&ta_empty[ab], (uint32_t)((it >> 1) & 1) ^ 1u);
-        ptx::tc_fence_after();
-        uint32_t hi[16], lo[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi[j]) : "f"(a[2 * j + 1]), "f"(a[2 * j]));
-          const float r0 = a[2 * j] - __uint_as_float(hi[j] << 16);
-          const float r1 = a[2 * j + 1] - __uint_as_float(hi[j] & 0xFFFF0000u);
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo[j]) : "f"(r1), "f"(r0));
-        }
-        const uint32_t ta = tmem_A + ab * 64 + (uint32_t)h * 16;
-        ptx::tmem_st16(ta + lane_off, hi);
-        ptx::tmem_st16(ta + lane_off + 32, lo);
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&ta_full[ab]);
-        (void)cv;
-      }
-    } else if (RL && warp >= K::W_CONV0 && warp < K::W_CONV0 + K::NCONVW) {
-      // ===================== RL: unswizzled K-chunk pair -> two SW128 K-major tiles =====================
-      // 16-byte piece q of the pair (vector v = q/16, piece c = q%16 of its 256 bytes) moves to
-      // tile c/8 (= ring slot rs + c/8), row v, SW128 position (c%8) ^ (v%8).  Reads: a warp
-      // reads 512 contiguous bytes; writes: 4 whole 128-byte rows.  In place, so everything
-      // is read (registers) before anything is written (named barrier).
-      const int cv = threadIdx.x - K::W_CONV0 * 32;
-      constexpr int NT = K::NCONVT;
-      constexpr int NIT = 2 * K::RAW_STAGE / 16 / NT;
-      static_assert(NIT * NT * 16 == 2 * K::RAW_STAGE, "re-layout tiling");
-      int rs = 0;
-      uint32_t rph = 0;
-      for (int64_t st = S0; st < S1; st += 2) {
-        ptx::mbar_wait(&raw_full[rs], rph);
-        uint8_t* base = smem + K::OFF_RAW + rs * K::RAW_STAGE;
-        const uint4* src = reinterpret_cast<const uint4*>(base);
-        uint4 a[NIT];
-#pragma unroll
-        for (int i = 0; i < NIT; ++i) a[i] = src[i * NT + cv];
-        ptx::named_bar_sync(2, NT);
-#pragma unroll
-        for (int i = 0; i < NIT; ++i) {
-          const uint32_t q = (uint32_t)(i * NT + cv), v = q >> 4, c = q & 15u;
-          *reinterpret_cast<uint4*>(base + (c >> 3) * K::RAW_STAGE + v * 128u + (((c & 7u) ^ (v & 7u)) << 4)) = a[i];
-        }
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&conv_full[rs]);
-        ptx::mbar_arrive(&conv_full[rs + 1]);
-        rs += 2;
-        if (rs == K::NRAW) rs = 0, rph ^= 1;
-      }
-    } else if (F32 && !TF && warp >= K::W_CONV0 && warp < K::W_CONV0 + 8) {
-      // ===================== fp32 -> (hi, lo) bf16 split =====================
-      // a = hi + lo, hi = bf16_rn(a), lo = bf16_rn(a - hi): |a - hi - lo| ≤ 2^-17 |a|.
-      // Thread cv owns 4 consecutive MN (or K) elements of rows cv/(BN/4) + RPI·i; the
-      // swizzled destination offset is affine in i, so it is precomputed (two parities).
-      const int cv = threadIdx.x - K::W_CONV0 * 32;
-      constexpr int NT = K::NCONVT;
-      constexpr int NIT = kBK * BN / 4 / NT;  // float4 per thread per stage
-      static_assert(NIT * NT * 4 == kBK * BN, "converter tiling");
-      // destination byte offset of iteration i = off_base[i & 1] + (i >> 1)·dstep (+ i·istep)
-      uint32_t off_even, off_odd, istep;
-      if (!TRANS) {
-        constexpr int F4R = BN / 4;     // float4 per data row
-        constexpr int RPI = NT / F4R;   // rows advanced per iteration (8 for BN=128, 16 for BN=64)
-        const int rowk0 = cv / F4R, c = (cv % F4R) * 4;
-        const int blk = c >> 6, cc = c & 63;
-        auto offr = [&](int rk) {
-          return (uint32_t)(blk * (kBK * 128) + (rk >> 3) * 1024 + (rk & 7) * 128 + (((cc >> 3) ^ (rk & 7)) << 4) +
-                            (cc & 7) * 2);
-        };
-        off_even = offr(rowk0);
-        off_odd = off_even;
-        istep = (uint32_t)(RPI / 8) * 1024u;  // RPI is a multiple of 8: (row & 7) is invariant
-      } else {
-        constexpr int RPI = NT / (kBK / 4);  // vectors advanced per iteration (16)
-        const int v0 = cv / (kBK / 4), c = (cv % (kBK / 4)) * 4;
-        off_even = (uint32_t)((v0 >> 3) * 1024 + (v0 & 7) * 128 + (((c >> 3) ^ (v0 & 7)) << 4) + (c & 7) * 2);
-        off_odd = off_even;
-        istep = (uint32_t)(RPI / 8) * 1024u;
-      }
-      (void)off_odd;
-      int rs = 0;
-      uint32_t rph = 0;
-      const int64_t total = S1 - S0;
-      const Tr tr((args.trace && cv == 0) ? args.trace + blockIdx.x * 16 : nullptr);
-      const unsigned long long tstart = tr.now();
-      for (int64_t it = 0; it < total; ++it) {
-        const unsigned long long t0 = tr.now();
-        ptx::mbar_wait(&raw_full[rs], rph);
-        tr.add(11, t0);
-        uint8_t* stage = smem + K::OFF_RAW + rs * K::RAW_STAGE;
-        const float4* rawp = reinterpret_cast<const float4*>(stage) + cv;
-        float4 a[NIT];
-#pragma unroll
-        for (int i = 0; i < NIT; ++i) a[i] = rawp[i * NT];
-        ptx::named_bar_sync(2, NT);  // every converter has read its part: the stage can be overwritten
-        uint8_t* hbase = stage + off_even;
-#pragma unroll
-        for (int i = 0; i < (BPS_DBG(2) ? 0 : NIT); ++i) {
-          uint32_t h01, h23, l01, l23;
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h01) : "f"(a[i].y), "f"(a[i].x));
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h23) : "f"(a[i].w), "f"(a[i].z));
-          const float r0 = a[i].x - __uint_as_float(h01 << 16), r1 = a[i].y - __uint_as_float(h01 & 0xFFFF0000u);
-          const float r2 = a[i].z - __uint_as_float(h23 << 16), r3 = a[i].w - __uint_as_float(h23 & 0xFFFF0000u);
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l01) : "f"(r1), "f"(r0));
-          asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l23) : "f"(r3), "f"(r2));
-          *reinterpret_cast<uint2*>(hbase + i * istep) = make_uint2(h01, h23);
-          *reinterpret_cast<uint2*>(hbase + K::CONV_HALF + i * istep) = make_uint2(l01, l23);
-        }
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&conv_full[rs]);
-        if (++rs == K::NRAW) rs = 0, rph ^= 1;
-      }
-      tr.add(12, tstart);
-    }
-  }
-  ptx::tc_fence_before();
-  if (CS > 1)
-    ptx::cluster_sync();  // no CTA leaves while peers may still copy into it or arrive on its barriers
-  else
-    __syncthreads();
-  if (warp == K::W_MMA) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, K::TMEM_COLS);
-  }
-}
-
-// Y += Y2 (balanced decomposition: the two parity buffers of split outputs; a fixed-order,
-// deterministic final combine).
-__global__ void __launch_bounds__(256) bps_add_kernel(float* __restrict__ Y, int64_t ldy, const float* __restrict__ Y2,
-                                                      int64_t ldy2, int64_t rows, int64_t cols) {
-  const int64_t c4 = (cols + 3) / 4;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * c4; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / c4, c = (e % c4) * 4;
-    float* y = Y + r * ldy + c;
-    const float* z = Y2 + r * ldy2 + c;
-    if (c + 4 <= cols) {
-      float4 a = *reinterpret_cast<float4*>(y);
-      const float4 b = *reinterpret_cast<const float4*>(z);
-      a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
-      *reinterpret_cast<float4*>(y) = a;
-    } else {
-      for (int64_t t = c; t < cols; ++t) Y[r * ldy + t] += Y2[r * ldy2 + t];
-    }
-  }
-}
-
-// ------------------------------------------------------------------ host side
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+// cuTensorMapEncodeTiled through the runtime's driver entry point; resolved once (thread-safe
+// function-local static initialisation)
+void* encode_tiled_entry() {
+  static void* fn = []() -> void* {
     cudaDriverEntryPointQueryResult q;
     void* f = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(f);
-  }
+      return f;
+    return nullptr;
+  }();
   return fn;
 }
 
-struct Plan {
+// per-launch flag nonce: a counter seeded from the clock, the process id and an address, mixed
+unsigned long long launch_nonce() {
+  static std::atomic<unsigned long long> ctr{mix64((unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count() ^
+                                                   ((unsigned long long)getpid() << 32) ^
+                                                   (unsigned long long)(uintptr_t)&ctr)};
+  return mix64(ctr.fetch_add(0x9E3779B97F4A7C15ull, std::memory_order_relaxed));
+}
+
+namespace {
+
+struct Coverage {
   bool ok = false;
   int nmt = 1;
-  int bn = 128;
   std::string why;
 };
 
-Plan plan_for(const SketchParams& p, bps_dtype dt) {
-  Plan pl;
+Coverage coverage(const SketchParams& p, bps_dtype dt) {
+  Coverage c;
   if (dt != BPS_F32 && dt != BPS_BF16) {
-    pl.why = "dtype";
-    return pl;
+    c.why = "dtype";
+    return c;
   }
   if (p.B_c % kBK != 0) {
-    pl.why = "tc variant needs B_c % 64 == 0";
-    return pl;
+    c.why = "tc variant needs B_c % 64 == 0";
+    return c;
   }
   const uint64_t rows = (uint64_t)p.kappa * p.B_r;
   if (rows > 512 || (rows > 256 && dt != BPS_BF16)) {
-    pl.why = "tc variant needs kappa*B_r <= 256 (fp32) or <= 512 (bf16)";
-    return pl;
+    c.why = "tc variant needs kappa*B_r <= 256 (fp32) or <= 512 (bf16)";
+    return c;
   }
   if ((uint64_t)p.kappa * p.s > 128) {
-    pl.why = "tc variant needs kappa*s <= 128";
-    return pl;
+    c.why = "tc variant needs kappa*s <= 128";
+    return c;
   }
   // more than 2 band tiles: rows ≥ 256 need the row-partitioned fast/dense generators (16-bit
   // stale-entry offsets), i.e. C = B_r/s a power of two and κs a multiple of 4
   if (rows > 256 && p.mode == 0 && ((p.C & (p.C - 1)) != 0 || ((uint64_t)p.kappa * p.s) % 4 != 0)) {
-    pl.why = "tc variant with kappa*B_r > 256 needs B_r/s a power of two and kappa*s % 4 == 0";
-    return pl;
+    c.why = "tc variant with kappa*B_r > 256 needs B_r/s a power of two and kappa*s % 4 == 0";
+    return c;
   }
-  // band M-tiles: 1, 2, or 4 (bf16 only: with BN = 64, D + S = 4·64 + 4·64 TMEM columns)
-  pl.nmt = rows <= 128 ? 1 : (rows <= 256 ? 2 : 4);
-  pl.ok = true;
-  return pl;
+  c.nmt = rows <= 128 ? 1 : (rows <= 256 ? 2 : 4);
+  c.ok = true;
+  return c;
 }
 
-// ranges per column tile: as many as fill the SMs, each ≥ κ-1 input blocks long so that
-// every split output has exactly two contributors (deterministic red.add, see header)
-int64_t ranges_for(const SketchParams& p, int64_t stream_len, int64_t n_ct, int sms) {
-  int64_t R = n_ct >= sms ? 1 : sms / n_ct;
-  if (R > stream_len) R = stream_len;
-  const int64_t need = p.kappa > 1 ? (int64_t)p.kappa - 1 : 1;
-  while (R > 1 && stream_len / R < need) --R;
-  return R;
-}
-
-template <typename Kern>
-void launch_cluster(Kern kern, unsigned grid, int threads, int smem, cudaStream_t st, int cs, const CUtensorMap& tm,
-                    const TcArgs& a) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = cs;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, tm, a);
-}
-
-template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF = false, bool RL = false>
-int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, float* Y, int64_t ldy,
-                const Placement& pl, float* Y2, int64_t ldy2, cudaStream_t st) {
-  using K = Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>;
-  constexpr int BN = K::BN;
-  EncodeTiledFn enc = encode_fn();
-  if (!enc) return fail(BPS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
-  TcArgs a;
-  a.p = p;
-  a.n = n;
-  a.Y = Y;
-  a.ldy = ldy;
-  a.range_mode = pl.range_mode;
-  a.pos_begin = pl.pos_begin;
-  a.pos_end = pl.pos_begin + pl.n_out;
-  int64_t in_rows;
-  if (pl.range_mode) {
-    a.stream_begin = pl.pos_begin + 1;
-    a.stream_len = pl.n_out + p.kappa - 1;
-    in_rows = a.stream_len * (int64_t)p.B_c;
-  } else {
-    a.stream_begin = 1;
-    a.stream_len = p.M;
-    in_rows = (int64_t)p.M * p.B_c;
-  }
-  // accumulation group: largest divisor of B_c/64 that is <= kMaxGroup K-chunks (precision)
+// K-chunks per accumulation group: the largest divisor of nk = B_c/64 not above the cap — 128
+// (precision: the tensor core's fp32 accumulate is not RN), or nk/2 (≤ 64) for
+// blocks of ≤ 128 chunks so that stream ranges can be balanced below one block.  A function of
+// the sketch only: the canonical fold of every output is fixed before any launch decision.
+int group_for(const SketchParams& p) {
   const int nk = (int)(p.B_c / kBK);
-  int G = 1;
-  for (int g = kMaxGroup; g >= 1; --g)
-    if (nk % g == 0) {
-      G = g;
-      break;
-    }
-  a.G = G;
-  a.dbg = 0;
-  a.trace = nullptr;
-  a.kgroup = 1;
-  if (const char* e = getenv("BPS_TC_KGROUP")) a.kgroup = atoi(e);  // tuning knob (transposed layout)
-  if (a.kgroup < 1) a.kgroup = 1;
-  if (a.kgroup > K::NRAW) a.kgroup = K::NRAW;  // a group must fit the ring (else the producer waits on itself)
-  if (!TRANS) {
-    // row-major: grouping only for the narrow bf16 tile (BPS_TC_KGROUP=2/4: 128/256-row boxes;
-    // measured no gain on smalln, off by default)
-    if (F32 || BN != 64 || (p.B_c / kBK) % a.kgroup || K::NRAW % a.kgroup || a.kgroup > 4 || (a.kgroup & (a.kgroup - 1)))
-      a.kgroup = 1;
-  }
-  a.nohoist = getenv("BPS_TC_NOHOIST") ? 1 : 0;
-  a.mma_hint = getenv("BPS_TC_MMA_HINT") ? (uint32_t)atoi(getenv("BPS_TC_MMA_HINT")) : 0u;  // A/B knob
-  a.tbox = BN;
-  if (const char* e = getenv("BPS_TC_TBOX")) a.tbox = atoi(e);  // tuning knob (transposed layout)
-  if (a.tbox < 8 || BN % a.tbox || a.tbox % 8 || a.kgroup == 1) a.tbox = BN;
-#ifdef BPS_TC_INSTRUMENT
-  {
-    const char* e = getenv("BPS_TC_DEBUG");
-    a.dbg = e ? atoi(e) : 0;
-  }
-#endif
-  if (const char* e = getenv("BPS_TC_GROUP")) {  // tuning knob: K-chunks per accumulation group
+  int cap = nk <= 128 ? std::max(1, std::min(64, nk / 2)) : 128;
+  if (const char* e = getenv("BPS_TC_GROUP")) {  // experiment knob (changes the canonical fold)
     const int g = atoi(e);
-    if (g >= 1 && nk % g == 0) a.G = g;
+    if (g >= 1 && nk % g == 0) return g;
   }
-  const int64_t n_ct = (n + BN - 1) / BN;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  auto kern = bps_tc_kernel<F32, TRANS, NMT, BN_, CS, TF, RL>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
-  if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-  if (CS > 1) {  // clusters must fit inside a GPC: not every SM can host one (e.g. 132 of 148 for 4-CTA clusters)
-    static int cached_slots[64] = {0};
-    int& slots = cached_slots[dev & 63];
-    if (!slots) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(CS * 64);
-      cfg.blockDim = dim3(K::NTHREADS);
-      cfg.dynamicSmemBytes = K::SMEM;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = CS;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      int clusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) clusters = sms / CS;
-      slots = clusters * CS;
-    }
-    sms = slots;
-  }
-  int64_t R;
-  a.balanced = Y2 != nullptr;
-  a.Y2 = Y2;
-  a.ldy2 = ldy2;
-  if (a.balanced) {
-    // stage-granular equal ranges: every range ≥ (κ·nk − 1)/3 stages, so an output window of
-    // κ·nk stages meets ≤ 4 ranges and each parity buffer receives ≤ 2 addends per element
-    const int64_t Ts = a.stream_len * nk, W = (int64_t)p.kappa * nk;
-    R = n_ct >= sms ? 1 : sms / n_ct;
-    if (R > Ts) R = Ts;
-    const int64_t U = RL ? 2 : ((!TRANS && a.kgroup > 1) ? a.kgroup : 1);  // range unit (stages)
-    while (R > 1 && U * (Ts / U / R) < (W - 1 + 2) / 3) --R;
-  } else {
-    R = ranges_for(p, a.stream_len, n_ct, sms);
-  }
-  a.R = (int)R;
-  a.nct = (int)n_ct;
-  const int64_t grid = n_ct * R;
-  if (grid > 0x7FFFFFFF) return fail(BPS_ERR_UNSUPPORTED, "grid too large");
-  if (in_rows > 0x7FFFFFFF || n > 0x7FFFFFFF) return fail(BPS_ERR_UNSUPPORTED, "tc variant: TMA coordinates exceed int32");
+  for (int g = cap; g >= 1; --g)
+    if (nk % g == 0) return g;
+  return 1;
+}
 
-  // TMA descriptor for the data operand
-  CUtensorMap tm;
-  const CUtensorMapDataType tdt = F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-  cuuint64_t dims[2], strides[1];
-  cuuint32_t box[2], estr[2] = {1, 1};
-  const CUtensorMapSwizzle swz = (F32 || RL) ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B;
-  strides[0] = (cuuint64_t)lda * K::ESZ;
-  if (!TRANS) {
-    dims[0] = (cuuint64_t)n;
-    dims[1] = (cuuint64_t)in_rows;
-    box[0] = F32 ? BN : 64;
-    box[1] = kBK * a.kgroup;
-  } else {
-    dims[0] = (cuuint64_t)in_rows;  // coordinates (d)
-    dims[1] = (cuuint64_t)n;        // vectors
-    box[0] = RL ? 2 * kBK : kBK;
-    box[1] = RL ? BN : a.tbox;
+int device_sms() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      sms <= 0) {
+    cudaGetLastError();
+    return 148;  // B200
   }
-  CUresult cr = enc(&tm, tdt, 2, const_cast<void*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return fail(BPS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+  return sms;
+}
 
-  // outputs split between CTAs are accumulated with red.add into zeroed buffers
-  const int64_t krows = pl.range_mode ? pl.n_out * (int64_t)p.B_r : (int64_t)p.M * p.B_r;
-  const int64_t yrows = TRANS ? n : krows, ycols = TRANS ? krows : n;
-  if (p.kappa > 1 || a.balanced) {
-    cudaError_t e = cudaMemset2DAsync(Y, ldy * 4, 0, (size_t)ycols * 4, (size_t)yrows, st);
-    if (e == cudaSuccess && a.balanced) e = cudaMemset2DAsync(Y2, ldy2 * 4, 0, (size_t)ycols * 4, (size_t)yrows, st);
-    if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaMemset2DAsync: ") + cudaGetErrorString(e));
+struct Choice {
+  bool f32, trans, tf, rl;
+  int nmt, bn, cs;
+};
+
+Choice choose(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl, int nmt, int sms,
+              bool canon, int G) {
+  Choice c{};
+  c.f32 = dt == BPS_F32;
+  c.trans = transposed;
+  c.nmt = nmt;
+  const int64_t n_out = pl.range_mode ? pl.n_out : (int64_t)p.M;
+  (void)n_out;
+  if (c.f32) {
+    c.bn = nmt == 1 ? 128 : 64;
+  } else if (nmt == 1) {
+    // bf16, one band tile: 256 columns per CTA (band reused over twice the columns) unless that
+    // leaves SMs idle, then 128; narrow row-major inputs take the 64-column tile with a deep ring
+    const int64_t ct256 = (n + 255) / 256, ct128 = (n + 127) / 128;
+    const int64_t used256 = ct256 >= sms ? ct256 : ct256 * (sms / ct256);
+    const int64_t used128 = ct128 >= sms ? ct128 : ct128 * (sms / ct128);
+    c.bn = (used256 * 10 >= used128 * 9 || used256 >= sms) ? 256 : 128;
+    if (n <= 64 && !transposed) c.bn = 64;
+    if (const char* e = getenv("BPS_TC_BN"))  // tuning knob
+      c.bn = atoi(e) == 128 ? 128 : (atoi(e) == 64 && !transposed ? 64 : 256);
+  } else {
+    c.bn = nmt == 2 ? 128 : 64;
   }
-#ifdef BPS_TC_INSTRUMENT
-  if (a.dbg & 8) {  // debug trace: per-CTA cycle counters, printed to stderr (synchronises)
-    cudaMalloc(&a.trace, (size_t)grid * 16 * 8);
-    cudaMemsetAsync(a.trace, 0, (size_t)grid * 16 * 8, st);
-  }
-  launch_cluster(kern, (unsigned)grid, K::NTHREADS, K::SMEM, st, CS, tm, a);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (a.trace) {
-    std::vector<unsigned long long> h((size_t)grid * 16);
-    cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    const char* names[13] = {"tma_wait_empty", "tma_total", "mma_wait_accfree", "mma_wait_data", "mma_wait_band",
-                             "mma_total", "band_wait_empty", "band_table", "band_total", "epi_wait_accfull",
-                             "epi_total", "conv_wait_raw", "conv_total"};
-    for (int k = 0; k < 13; ++k) {
-      double sum = 0, mx = 0;
-      for (int64_t c = 0; c < grid; ++c) {
-        sum += (double)h[c * 16 + k];
-        mx = std::max(mx, (double)h[c * 16 + k]);
-      }
-      fprintf(stderr, "[bps trace] %-18s mean %12.0f  max %12.0f cycles\n", names[k], sum / grid, mx);
-    }
-    cudaFree(a.trace);
-  }
-#else
-  launch_cluster(kern, (unsigned)grid, K::NTHREADS, K::SMEM, st, CS, tm, a);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-#endif
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("bps_tc_kernel launch: ") + cudaGetErrorString(e));
-  if (a.balanced) {
-    const int64_t work = yrows * ((ycols + 3) / 4);
-    const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)sms * 8);
-    bps_add_kernel<<<blocks, 256, 0, st>>>(Y, ldy, Y2, ldy2, yrows, ycols);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("bps_add_kernel launch: ") + cudaGetErrorString(e));
-  }
-  return BPS_OK;
+  c.tf = c.f32 && !transposed && nmt == 1;
+  // bf16 transposed, one band tile: 256-byte K-chunk pairs + in-smem re-layout; ranges must be whole
+  // pairs (canon: G even)
+  c.rl = !c.f32 && transposed && nmt == 1 && (p.B_c % (2 * kBK)) == 0 && (!canon || G % 2 == 0) &&
+         !(getenv("BPS_TC_RL") && atoi(getenv("BPS_TC_RL")) == 0);
+  const char* cse = getenv("BPS_TC_CLUSTER");  // tuning knob: 1 (off) or 2 CTAs sharing the band
+  int cs = cse ? atoi(cse) : (nmt == 4 ? 1 : 2);  // nmt 4: 64 KB band stages, no cluster (measured 2.1x)
+  if (cs != 1 && cs != 2) cs = 2;
+  const int64_t nct = (n + c.bn - 1) / c.bn;
+  while (cs > 1 && nct % cs) cs /= 2;
+  c.cs = cs;
+  return c;
 }
 
 }  // namespace
 
-int tc_supported(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl) {
-  (void)n;
+int supported_impl(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl) {
   (void)transposed;
-  (void)pl;
-  Plan plan = plan_for(p, dt);
-  if (!plan.ok) return fail(BPS_ERR_UNSUPPORTED, plan.why);
+  Coverage cv = coverage(p, dt);
+  if (!cv.ok) return fail(BPS_ERR_UNSUPPORTED, cv.why);
+  const int64_t in_rows = (pl.range_mode ? pl.n_out + (int64_t)p.kappa - 1 : (int64_t)p.M) * (int64_t)p.B_c;
+  if (in_rows > 0x7FFFFFFF || n > 0x7FFFFFFF)
+    return fail(BPS_ERR_UNSUPPORTED, "tc variant: TMA coordinates exceed int32 (d or n >= 2^31)");
   return BPS_OK;
 }
 
-size_t tc_workspace_bytes(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl) {
-  if (!plan_for(p, dt).ok) return 0;
-  const int64_t krows = pl.range_mode ? pl.n_out * (int64_t)p.B_r : (int64_t)p.M * p.B_r;
-  const int64_t rows = transposed ? n : krows, cols = transposed ? krows : n;
-  return (size_t)rows * (size_t)((cols + 3) / 4 * 4) * 4;
+size_t workspace_impl(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl) {
+  Coverage cv = coverage(p, dt);
+  if (!cv.ok || n <= 0) return 0;
+  const int sms = device_sms();
+  const int G = group_for(p);
+  const Choice c = choose(p, n, dt, transposed, pl, cv.nmt, sms, true, G);
+  const int64_t nct = (n + c.bn - 1) / c.bn;
+  const int64_t ctas = std::max<int64_t>(nct, sms);  // grid = nct·R ≤ max(nct, co-resident slots)
+  return kWsHeader + round256((size_t)ctas * p.kappa * 8) +
+         (size_t)ctas * (size_t)tiles_per_cta(p, G) * p.B_r * c.bn * 4;
 }
 
+int launch_tc_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt, float* Y, int64_t ldy,
+              bool transposed, const Placement& pl, void* ws, size_t ws_bytes, cudaStream_t st) {
+  Coverage cv = coverage(p, dt);
+  if (!cv.ok) return fail(BPS_ERR_UNSUPPORTED, cv.why);
+  HostPlan hp{};
+  hp.sms = device_sms();
+  hp.G = group_for(p);
+  const size_t need = workspace_impl(p, n, dt, transposed, pl);
+  hp.canon = ws && need && ws_bytes >= need && ((uintptr_t)ws % 256) == 0;
+  hp.ws = hp.canon ? ws : nullptr;
+  hp.ws_bytes = hp.canon ? ws_bytes : 0;
+  const Choice c = choose(p, n, dt, transposed, pl, cv.nmt, hp.sms, hp.canon, hp.G);
+#define BPS_TC_MATCH(F, T, NM, B, C, TF_, RL_)                                                                \
+  if (c.f32 == F && c.trans == T && c.nmt == NM && c.bn == B && c.cs == C && c.tf == TF_ && c.rl == RL_) \
+    return launch_impl<F, T, NM, B, C, TF_, RL_>(p, A, lda, n, Y, ldy, pl, hp, st);
+  BPS_TC_INSTANTIATIONS(BPS_TC_MATCH)
+#undef BPS_TC_MATCH
+  return fail(BPS_ERR_UNSUPPORTED, "no tc instantiation for this plan");
+}
+
+}  // namespace tcx
+
+int tc_supported(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl) {
+  return tcx::supported_impl(p, n, dt, transposed, pl);
+}
+size_t tc_workspace_bytes(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl) {
+  return tcx::workspace_impl(p, n, dt, transposed, pl);
+}
 int launch_tc(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt, float* Y, int64_t ldy,
               bool transposed, const Placement& pl, void* ws, size_t ws_bytes, cudaStream_t st) {
-  float* Y2 = nullptr;
-  int64_t ldy2 = 0;
-  const size_t need = tc_workspace_bytes(p, n, dt, transposed, pl);
-  // the balanced decomposition only pays when whole-block ranges are uneven (e.g. LS: 128 blocks
-  // over 37 ranges = 3 or 4 blocks); it costs two memsets and an add pass otherwise
-  bool uneven = false;
-  if (ws) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const Plan pln = plan_for(p, dt);
-    const int bnx = (dt == BPS_F32) ? (pln.nmt == 1 ? 128 : 64) : 128;  // conservative (smaller) tile
-    const int64_t sl = pl.range_mode ? pl.n_out + p.kappa - 1 : (int64_t)p.M;
-    const int64_t nct = (n + bnx - 1) / bnx;
-    const int64_t R = ranges_for(p, sl, nct, sms);
-    const int64_t Lmax = (sl + R - 1) / R;
-    uneven = R > 1 && (double)Lmax * R > 1.05 * (double)sl;
-  }
-  if (ws && uneven && need && ws_bytes >= need && ((uintptr_t)ws % 16) == 0) {
-    const int64_t krows = pl.range_mode ? pl.n_out * (int64_t)p.B_r : (int64_t)p.M * p.B_r;
-    Y2 = (float*)ws;
-    ldy2 = ((transposed ? krows : n) + 3) / 4 * 4;
-  }
-  Plan plan = plan_for(p, dt);
-  if (!plan.ok) return fail(BPS_ERR_UNSUPPORTED, plan.why);
-  const bool f32 = dt == BPS_F32;
-  // bf16, one M-tile: 256 columns per CTA (band reused over twice the columns) unless that
-  // leaves SMs idle, then 128.
-  int bn = 128;
-  if (!f32 && plan.nmt == 1) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t sl = pl.range_mode ? pl.n_out + p.kappa - 1 : (int64_t)p.M;
-    const int64_t ct256 = (n + 255) / 256, ct128 = (n + 127) / 128;
-    const int64_t used256 = ct256 * ranges_for(p, sl, ct256, sms);
-    const int64_t used128 = ct128 * ranges_for(p, sl, ct128, sms);
-    bn = (used256 * 10 >= used128 * 9 || used256 >= sms) ? 256 : 128;
-    if (n <= 64 && !transposed) bn = 64;  // narrow inputs: half the MMA/smem work of a 128 tile, deeper ring
-    if (const char* e = getenv("BPS_TC_BN")) bn = atoi(e) == 128 ? 128 : (atoi(e) == 64 && !transposed ? 64 : 256);  // tuning knob
-  }
-  // share band generation across a 4-CTA cluster when the column tiles come in fours
-  const int bnsel = (f32 && plan.nmt == 2) ? 64 : bn;
-  const int64_t nct_sel = (n + bnsel - 1) / bnsel;
-  const char* cse = getenv("BPS_TC_CLUSTER");  // tuning knob: 1 (off), 2 or 4 CTAs sharing the band
-  int cs = cse ? atoi(cse) : 2;
-  if (cs != 1 && cs != 2 && cs != 4) cs = 2;
-  while (cs > 1 && nct_sel % cs) cs /= 2;
-#define BPS_TC_CASE(F, T, NM, B)                                                                  \
-  if (f32 == F && transposed == T && plan.nmt == NM && bn == B)                                   \
-    return cs == 4   ? launch_impl<F, T, NM, B, 4>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st)        \
-           : cs == 2 ? launch_impl<F, T, NM, B, 2>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st)        \
-                     : launch_impl<F, T, NM, B, 1>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st);
-  // bf16 transposed layout, one band tile: 256-byte K-chunk pairs + in-smem re-layout (RL)
-  // (BPS_TC_RL=0: plain SW128 boxes of 128-byte runs); clusters of at most 2
-  if (!f32 && transposed && plan.nmt == 1 && (p.B_c % (2 * kBK)) == 0 &&
-      !(getenv("BPS_TC_RL") && atoi(getenv("BPS_TC_RL")) == 0)) {
-    if (cs > 2) cs = 2;
-    if (bn == 256)
-      return cs == 2 ? launch_impl<false, true, 1, 256, 2, false, true>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st)
-                     : launch_impl<false, true, 1, 256, 1, false, true>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st);
-    return cs == 2 ? launch_impl<false, true, 1, 128, 2, false, true>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st)
-                   : launch_impl<false, true, 1, 128, 1, false, true>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st);
-  }
-  // fp32 row-major, one band tile: transposed MMA form (data in TMEM) unless BPS_TC_FORM=nt
-  if (f32 && !transposed && plan.nmt == 1 && !(getenv("BPS_TC_FORM") && getenv("BPS_TC_FORM")[0] == 'n'))
-    return cs == 4   ? launch_impl<true, false, 1, 128, 4, true>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st)
-           : cs == 2 ? launch_impl<true, false, 1, 128, 2, true>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st)
-                     : launch_impl<true, false, 1, 128, 1, true>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st);
-  BPS_TC_CASE(true, false, 1, 128)
-  BPS_TC_CASE(true, true, 1, 128)
-  if (f32) bn = 64;
-  BPS_TC_CASE(true, false, 2, 64)
-  BPS_TC_CASE(true, true, 2, 64)
-  BPS_TC_CASE(false, false, 1, 256)
-  BPS_TC_CASE(false, true, 1, 256)
-  BPS_TC_CASE(false, false, 1, 128)
-  BPS_TC_CASE(false, false, 1, 64)
-  BPS_TC_CASE(false, true, 1, 128)
-  BPS_TC_CASE(false, false, 2, 128)
-  if (plan.nmt == 4) {  // bf16, κ·B_r ≤ 512: 64-column tiles; 64 KB band stages, so a 2-CTA cluster
-    // leaves each CTA one local band buffer: no cluster by default (measured 2.1× faster at κs = 16)
-    bn = 64;
-    cs = cse ? atoi(cse) : 1;
-    if (cs != 1 && cs != 2) cs = 2;
-    while (cs > 1 && ((n + 63) / 64) % cs) cs /= 2;
-  }
-  if (!f32 && plan.nmt == 4) {
-    if (transposed)
-      return cs == 2 ? launch_impl<false, true, 4, 64, 2>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st)
-                     : launch_impl<false, true, 4, 64, 1>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st);
-    return cs == 2 ? launch_impl<false, false, 4, 64, 2>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st)
-                   : launch_impl<false, false, 4, 64, 1>(p, A, lda, n, Y, ldy, pl, Y2, ldy2, st);
-  }
-  BPS_TC_CASE(false, true, 2, 128)
-#undef BPS_TC_CASE
-  return fail(BPS_ERR_UNSUPPORTED, "no tc instantiation for this plan");
+  return tcx::launch_tc_impl(p, A, lda, n, dt, Y, ldy, transposed, pl, ws, ws_bytes, st);
 }
 
 }  // namespace bps

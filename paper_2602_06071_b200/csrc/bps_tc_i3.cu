@@ -1,0 +1,8 @@
+// bps_tc_i3.cu — explicit instantiations 4/8 of the tcgen05 kernel (bps_tc_kernel.cuh),
+// split across units so that nvcc compiles them in parallel.
+#include "bps_tc_kernel.cuh"
+
+BPS_TC_DEFINE(true, true, 1, 128, 2, false, false)
+BPS_TC_DEFINE(false, false, 1, 128, 2, false, false)
+BPS_TC_DEFINE(false, true, 1, 256, 2, false, false)
+BPS_TC_DEFINE(false, false, 4, 64, 2, false, false)

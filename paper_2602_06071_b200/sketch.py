@@ -103,14 +103,27 @@ class Sketch:
             cache[key] = b.value
         return cache[key]
 
-    def _workspace(self, n, dtype_code, transposed, device, use_workspace):
-        """Scratch for the balanced tc decomposition, from torch's caching allocator."""
+    def _scratch(self, nbytes: int, device):
+        """One workspace per device, grown on demand; its 256-byte header is zeroed once at
+        allocation (bps.h: the library keeps it valid across calls).  A Sketch must not run two
+        applies concurrently on different streams (they would share this workspace)."""
         import torch
 
-        nbytes = self.workspace_bytes(n, dtype_code, transposed) if use_workspace and hasattr(lib, "bps_workspace_size") else 0
         if not nbytes:
             return None, 0
-        return torch.empty(nbytes, dtype=torch.uint8, device=device), nbytes
+        bufs = self.__dict__.setdefault("_ws_bufs", {})
+        key = (device.type, device.index if device.index is not None else torch.cuda.current_device())
+        buf = bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            buf[:256].zero_()
+            bufs[key] = buf
+        return buf, buf.numel()
+
+    def _workspace(self, n, dtype_code, transposed, device, use_workspace):
+        """Scratch for the full-occupancy tc decomposition (bps_apply_ws)."""
+        nbytes = self.workspace_bytes(n, dtype_code, transposed) if use_workspace else 0
+        return self._scratch(nbytes, device)
 
     def pattern(self, g: int, ell: int, u: int, j: int) -> tuple[int, int]:
         r, sg = ctypes.c_int32(), ctypes.c_int32()
@@ -183,8 +196,10 @@ class Sketch:
                                  VARIANTS[variant]))
         return out
 
-    def apply_orbit_range(self, pos_begin: int, pos_end: int, A_local, out=None, variant: str = "auto"):
-        """Partial apply over orbit positions [pos_begin, pos_end) (bps_apply_orbit_range)."""
+    def apply_orbit_range(self, pos_begin: int, pos_end: int, A_local, out=None, variant: str = "auto",
+                          use_workspace: bool = True):
+        """Partial apply over orbit positions [pos_begin, pos_end) (bps_apply_orbit_range_ws): the
+        output blocks at those positions, stacked, bitwise equal to the matching rows of apply()."""
         import torch
 
         _check_matrix(A_local, "A_local")
@@ -194,9 +209,19 @@ class Sketch:
         n = A_local.shape[1]
         if out is None:
             out = torch.empty((L * self.B_r, n), dtype=torch.float32, device=A_local.device)
-        check(lib.bps_apply_orbit_range(self._h, pos_begin, pos_end, A_local.data_ptr(), A_local.stride(0), n,
-                                        _dtype_code(A_local), out.data_ptr(), out.stride(0),
-                                        _stream_ptr(A_local.device), VARIANTS[variant]))
+        _check_matrix(out, "out")
+        if out.dtype != torch.float32 or tuple(out.shape) != (L * self.B_r, n) or out.device != A_local.device:
+            raise ValueError("out must be float32 (L*B_r)×n on the device of A_local")
+        code = _dtype_code(A_local)
+        nbytes = 0
+        if use_workspace:
+            b = ctypes.c_size_t()
+            check(lib.bps_orbit_range_workspace_size(self._h, pos_begin, pos_end, n, code, ctypes.byref(b)))
+            nbytes = b.value
+        ws, wsb = self._scratch(nbytes, A_local.device)
+        check(lib.bps_apply_orbit_range_ws(self._h, pos_begin, pos_end, A_local.data_ptr(), A_local.stride(0), n, code,
+                                           out.data_ptr(), out.stride(0), ws.data_ptr() if ws is not None else None,
+                                           wsb, _stream_ptr(A_local.device), VARIANTS[variant]))
         return out
 
     def apply_raw(self, A_ptr: int, lda: int, n: int, dtype_code: int, Y_ptr: int, ldy: int, stream: int,

@@ -188,25 +188,30 @@ def test_zero_n_and_zero_input():
 
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_orbit_range_matches_full(variant):
-    """bps_apply_orbit_range over [p0,p1) on stacked input blocks = the matching rows of
-    the full apply (DESIGN.md §7 block sharding)."""
+    """bps_apply_orbit_range over [p0,p1) on stacked input blocks = the matching rows of the
+    full apply of the same variant, bit for bit (R19; DESIGN.md §7 block sharding), and the
+    oracle's rows per column (tests/test_gpu_sharding.py has the full sweep)."""
     M, Br, Bc, kappa, s = 16, 32, 256, 4, 2
     sk, osk = _pair(M, Br, Bc, kappa, s, seed=8)
     n = 64
-    A = torch.randn((sk.d, n), device="cuda")
-    Yfull = sk.apply(A, variant="sparse")
+    A_h = synth.host_matrix("gaussian", sk.d, n, seed=8)
+    A = torch.from_numpy(A_h).cuda()
+    try:
+        Yfull = sk.apply(A, variant=variant)
+    except BpsError as e:
+        if e.code == -3 and variant == "tc":
+            pytest.skip(str(e))
+        raise
     orb = sk.orbit()
+    nrm = np.linalg.norm(A_h.astype(np.float64), axis=0)
     for (p0, p1) in [(0, 16), (3, 9), (13, 20), (15, 16)]:
         blocks = [orb[(p % M)] for p in range(p0 + 1, p1 + kappa)]
         A_loc = torch.cat([A[h * Bc:(h + 1) * Bc] for h in blocks])
-        try:
-            Y_loc = sk.apply_orbit_range(p0, p1, A_loc, variant=variant)
-        except BpsError as e:
-            if e.code == -3 and variant == "tc":
-                pytest.skip(str(e))
-            raise
+        Y_loc = sk.apply_orbit_range(p0, p1, A_loc, variant=variant)
         ref = torch.cat([Yfull[orb[p % M] * Br:(orb[p % M] + 1) * Br] for p in range(p0, p1)])
-        assert torch.allclose(Y_loc, ref, rtol=0, atol=1e-5 * float(A.norm(dim=0).max())), (p0, p1)
+        assert torch.equal(Y_loc, ref), (p0, p1)
+        assert_f32(Y_loc.cpu().numpy(), oracle.apply(osk, A_h, blocks=[orb[p % M] for p in range(p0, p1)]), nrm,
+                   f"orbit [{p0},{p1}) {variant}")
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -288,14 +293,16 @@ def test_sweep_sampled(cfg):
     _sampled_check(cfg, "auto")
 
 
-# ------------------------------------- balanced (workspace) vs block-aligned decomposition
+# ------------------------------------- workspace (stream ranges) vs halo-range decomposition
 @pytest.mark.parametrize("layout,n,dt", [((128, 32, 8192, 4, 4), 512, "f32"), ((16, 32, 1024, 4, 4), 200, "f32"),
                                          ((64, 16, 512, 8, 2), 304, "bf16"), ((16, 16, 256, 1, 4), 64, "f32"),
-                                         ((8, 32, 128, 8, 2), 48, "bf16")])
+                                         ((8, 32, 128, 8, 2), 40, "bf16"), ((8, 32, 128, 8, 2), 48, "bf16"),
+                                         ((7, 32, 64, 4, 4), 64, "f32")])
 @pytest.mark.parametrize("transposed", [False, True])
-def test_balanced_decomposition(layout, n, dt, transposed):
-    """Stage-granular ranges with the parity workspace (bps_apply_ws) agree with the oracle and
-    are bitwise reproducible; the block-aligned path (no workspace) agrees too."""
+def test_workspace_decomposition(layout, n, dt, transposed):
+    """Group-aligned stream ranges with the owner/contributor workspace (bps_apply_ws) agree with
+    the oracle, are bitwise reproducible and bitwise equal to the no-workspace (halo) ranges.
+    (7, 32, 64, 4, 4): odd M, the shape ADVICE r1 found breaking the old parity routing."""
     sk, osk = _pair(*layout, seed=17)
     tdt = torch.float32 if dt == "f32" else torch.bfloat16
     A = synth.host_matrix("gaussian", sk.d, n, seed=4)
@@ -317,6 +324,7 @@ def test_balanced_decomposition(layout, n, dt, transposed):
         Yn = Y.cpu().numpy()
         outs.append(Yn.T if transposed else Yn)
     assert np.array_equal(outs[0], outs[1])  # bitwise reproducible
+    assert np.array_equal(outs[0], outs[2])  # bitwise independent of the decomposition
     for Y in outs:
         assert_f32(Y, ref, nrm, f"{layout} n={n} {dt} T={transposed}")
 
