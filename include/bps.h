@@ -135,15 +135,15 @@ int bps_apply_t_ex(const bps_sketch* sk, const void* X, int64_t ldx, int64_t n, 
 /*
  * Workspace forms (the full-occupancy tc path; the Python binding always uses them).  With a
  *   device workspace of at least bps_workspace_size() bytes the tc variant splits the input
- *   stream into equal group-aligned ranges, one CTA (pair) per SM: the CTA holding an output's
- *   first accumulation group finishes it, in stream order, from the group partials that the CTAs
- *   holding its later groups leave in the workspace (epoch-tagged flags, no atomics on Y).  The
- *   result is bitwise identical to the no-workspace call (see bps_apply).
- *   Workspace: caller-owned device memory, 256-byte aligned, not overlapping the output; its
- *   FIRST 256 BYTES MUST BE ZERO before its first use (e.g. cudaMemset once at allocation); each
- *   call leaves them valid for the next, so no re-zeroing is needed between calls.  One workspace
- *   must not be used by two calls that may run concurrently.  A too small workspace (or NULL) is
- *   ignored (no-workspace behaviour).  bytes = 0: the shape has no tc plan (sparse kernel).
+ *   stream into equal group-aligned ranges, one CTA (pair) per SM; a CTA holding later
+ *   accumulation groups of an output that straddles a range boundary leaves their partial sums
+ *   in the workspace, and a second small kernel adds them, in stream order, onto the prefix the
+ *   first CTA left in Y (no atomics, no pre-zeroing).  The result is bitwise identical to the
+ *   no-workspace call (see bps_apply).
+ *   Workspace: caller-owned device memory, 256-byte aligned, not overlapping the output; pure
+ *   scratch (no initialisation needed, contents undefined afterwards).  One workspace must not be
+ *   used by two calls that may run concurrently.  A too small workspace (or NULL) is ignored
+ *   (no-workspace behaviour).  bytes = 0: the shape has no tc plan (sparse kernel).
  */
 int bps_workspace_size(const bps_sketch* sk, int64_t n, bps_dtype dtype, int transposed, size_t* bytes);
 int bps_apply_ws(const bps_sketch* sk, const void* A, int64_t lda, int64_t n, bps_dtype dtype,

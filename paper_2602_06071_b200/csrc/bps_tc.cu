@@ -10,11 +10,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-#include <unistd.h>
-
 #include <algorithm>
-#include <atomic>
-#include <chrono>
 #include <cstdlib>
 #include <string>
 
@@ -35,14 +31,6 @@ void* encode_tiled_entry() {
     return nullptr;
   }();
   return fn;
-}
-
-// per-launch flag nonce: a counter seeded from the clock, the process id and an address, mixed
-unsigned long long launch_nonce() {
-  static std::atomic<unsigned long long> ctr{mix64((unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count() ^
-                                                   ((unsigned long long)getpid() << 32) ^
-                                                   (unsigned long long)(uintptr_t)&ctr)};
-  return mix64(ctr.fetch_add(0x9E3779B97F4A7C15ull, std::memory_order_relaxed));
 }
 
 namespace {
@@ -171,8 +159,7 @@ size_t workspace_impl(const SketchParams& p, int64_t n, bps_dtype dt, bool trans
   const Choice c = choose(p, n, dt, transposed, pl, cv.nmt, sms, true, G);
   const int64_t nct = (n + c.bn - 1) / c.bn;
   const int64_t ctas = std::max<int64_t>(nct, sms);  // grid = nct·R ≤ max(nct, co-resident slots)
-  return kWsHeader + round256((size_t)ctas * p.kappa * 8) +
-         (size_t)ctas * (size_t)tiles_per_cta(p, G) * p.B_r * c.bn * 4;
+  return (size_t)ctas * (size_t)tiles_per_cta(p, G) * p.B_r * c.bn * 4;
 }
 
 int launch_tc_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt, float* Y, int64_t ldy,
@@ -183,7 +170,9 @@ int launch_tc_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n,
   hp.sms = device_sms();
   hp.G = group_for(p);
   const size_t need = workspace_impl(p, n, dt, transposed, pl);
-  hp.canon = ws && need && ws_bytes >= need && ((uintptr_t)ws % 256) == 0;
+  // canon needs the workspace; an output's group partials must fit the combine kernel's tile list
+  hp.canon = ws && need && ws_bytes >= need && ((uintptr_t)ws % 256) == 0 &&
+             (int64_t)p.kappa * ((p.B_c / kBK) / hp.G) <= 1024;
   hp.ws = hp.canon ? ws : nullptr;
   hp.ws_bytes = hp.canon ? ws_bytes : 0;
   const Choice c = choose(p, n, dt, transposed, pl, cv.nmt, hp.sms, hp.canon, hp.G);

@@ -14,10 +14,10 @@ constexpr int kBK = 64;  // K rows (input rows u) per pipeline stage
 // Everything the host decided before choosing a template instantiation.
 struct HostPlan {
   int G;            // K-chunks per accumulation group: a function of the sketch only (canonical sums)
-  int canon;        // 1: ranges partition the input stream, straddling outputs finished by their owner
-                    //    from contributors' group partials in the workspace; 0: "halo" ranges (each CTA
-                    //    streams the κ-window of its own outputs, no workspace)
-  void* ws;         // canon: workspace (header, flags, partial tiles)
+  int canon;        // 1: ranges partition the input stream; straddling outputs are finished by
+                    //    bps_tc_combine from the group partials in the workspace; 0: "halo" ranges (each
+                    //    CTA streams the κ-window of its own outputs, no workspace)
+  void* ws;         // canon: workspace (group-partial tiles; scratch)
   size_t ws_bytes;
   int sms;          // multiprocessor count of the current device
 };
@@ -66,10 +66,7 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
 BPS_TC_INSTANTIATIONS(BPS_TC_DECLARE)
 #undef BPS_TC_DECLARE
 
-// canonical workspace layout (bytes): [0, 256) header {epoch, done}; [256, 256 + F) flags
-// (uint64 per (CTA, straddler j)); then the partial tiles (B_r × BN fp32 each)
-constexpr size_t kWsHeader = 256;
-inline size_t round256(size_t x) { return (x + 255) / 256 * 256; }
+// canonical workspace: the partial tiles (B_r × BN fp32 each), tiles_per_cta per CTA; pure scratch
 // tiles each CTA may write: straddler j (0..κ-1) contributes at most (j+1)·nk/G groups
 inline int64_t tiles_per_cta(const SketchParams& p, int G) {
   const int64_t npg = (int64_t)(p.B_c / kBK) / G;

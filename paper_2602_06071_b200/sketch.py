@@ -104,9 +104,8 @@ class Sketch:
         return cache[key]
 
     def _scratch(self, nbytes: int, device):
-        """One workspace per device, grown on demand; its 256-byte header is zeroed once at
-        allocation (bps.h: the library keeps it valid across calls).  A Sketch must not run two
-        applies concurrently on different streams (they would share this workspace)."""
+        """One scratch workspace per device, grown on demand (bps.h: no initialisation needed).
+        A Sketch must not run two applies concurrently on different streams (they would share it)."""
         import torch
 
         if not nbytes:
@@ -116,7 +115,6 @@ class Sketch:
         buf = bufs.get(key)
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-            buf[:256].zero_()
             bufs[key] = buf
         return buf, buf.numel()
 

@@ -9,4 +9,4 @@ for c in ${CFGS:-ls grad}; do
   BARGS="--config $c" b ${c}_g128 BPS_TC_GROUP=128
   BARGS="--config $c" b ${c}_old BPS_LIB=$PWD/ab_old/libbps_old.so
 done
-timeout 300 python scripts/tc_trace.py ${CFGS:-ls grad} > $O/${T}_trace.txt 2>&1; echo trace rc=$?; cat $O/${T}_trace.txt | head -40
+timeout 300 python scripts/tc_trace.py ${CFGS:-ls grad} > $O/${T}_trace.txt 2>&1; echo trace rc=$?; cat $O/${T}_trace.txt | head -40; BPS_LIB=$PWD/ab_old/libbps_old_instr.so timeout 300 python scripts/tc_trace.py ${CFGS:-ls grad} > $O/${T}_trace_old.txt 2>&1; head -16 $O/${T}_trace_old.txt
