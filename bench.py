@@ -40,8 +40,10 @@ def parse():
     ap.add_argument("--variant", default="auto", choices=["auto", "sparse", "tc"])
     ap.add_argument("--kind", default="gaussian", choices=["gaussian", "coherent", "lowrank"])
     ap.add_argument("--shard", default="column", choices=["column", "block"],
-                    help="column: weak scaling, every rank its own n-column batch (no collective); "
-                         "block: strong scaling of one d×n problem sharded along the wiring orbit + all-gather")
+                    help="column: weak scaling, every rank its own n-column batch (no collective; at N>1 the "
+                         "line also carries the strong-scaling measurement: the config's n split over the "
+                         "ranks with dist.column_shard); block: strong scaling of one d×n problem sharded along "
+                         "the wiring orbit + all-gather")
     ap.add_argument("--op", default="apply", choices=["apply", "adjoint"],
                     help="adjoint: X = Sᵀ·Y (fp32 k×n -> d×n) on the same sketch; secondary line, no e2e/cpu legs")
     ap.add_argument("--sketch", default="blockperm", choices=["blockperm", "blockrow"],
@@ -53,6 +55,9 @@ def parse():
                     help="t: transposed layout (bps_apply_t, §8a8): X = Aᵀ n×d row-major in, Yᵀ n×k out")
     ap.add_argument("--t-pad", type=int, default=0, help=argparse.SUPPRESS)  # experiment: ldx = d + pad (transposed)
     ap.add_argument("--no-workspace", action="store_true", help="block-aligned ranges (no balanced workspace)")
+    ap.add_argument("--ref-cols", type=int, default=64, help="reference arm: columns of the oracle sample per step")
+    ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)  # launcher test without a GPU
+    ap.add_argument("--no-strong", action="store_true", help="N>1 column mode: skip the strong-scaling measurement")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -126,45 +131,77 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_baseline(cfg, n_sample, min_seconds=10.0, max_repeats=8):
-    """Time the oracle as it stands on a bounded column sample (rank 0, N=1): repeated until about
-    min_seconds of CPU work (at least 2, at most max_repeats runs), median reported."""
+# ------------------------------------------------------------------ the CPU oracle as a baseline
+_POOL_STATE = {}
+
+
+def _oracle_panel(cols):
+    """Worker: the oracle's product S @ A64 on a column panel (fork-inherited S and A)."""
+    import numpy as np
+
+    S, A = _POOL_STATE["S"], _POOL_STATE["A"]
+    return S @ np.asarray(A[:, cols[0]:cols[1]], dtype=np.float64)
+
+
+def oracle_timing(cfg, n_sample, cores=None, repeats=1):
+    """Time the oracle as it stands (oracle.build_S_csr, then the CSR product oracle.apply performs)
+    on an n_sample-column sample of the config, over all host cores: S built once per repeat
+    (timed), the product split into column panels over a fork pool with one BLAS thread per worker
+    (timed).  Returns dict(build_s, multiply_s, cores, n)."""
+    import multiprocessing as mp
+
     import numpy as np
 
     import oracle
     import synth
 
+    cores = cores or len(os.sched_getaffinity(0))
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
     osk = oracle.make_sketch(cfg.M, cfg.B_r, cfg.B_c, cfg.kappa, cfg.s, cfg.seed)
     A = synth.host_matrix("gaussian", cfg.d, n_sample, seed=3, dtype=np.float32)
-    times = []
-    while (len(times) < 2 and sum(times) < 15.0) or (sum(times) < min_seconds and len(times) < max_repeats):
+    nw = max(1, min(cores, n_sample))
+    panels = [(n_sample * w // nw, n_sample * (w + 1) // nw) for w in range(nw)]
+    builds, mults = [], []
+    for _ in range(repeats):
         t0 = time.perf_counter()
-        oracle.apply(osk, A)
-        times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
-    return t, cfg.roofline_bytes(n_sample), len(times)
+        S = oracle.build_S_csr(osk)
+        builds.append(time.perf_counter() - t0)
+        _POOL_STATE.update(S=S, A=A)
+        with mp.get_context("fork").Pool(nw) as pool:
+            t0 = time.perf_counter()
+            parts = pool.map(_oracle_panel, panels)
+            mults.append(time.perf_counter() - t0)
+        assert sum(x.shape[1] for x in parts) == n_sample
+        _POOL_STATE.clear()
+    return {"build_s": statistics.median(builds), "multiply_s": statistics.median(mults), "cores": nw, "n": n_sample}
+
+
+def oracle_fits(cfg):
+    # the oracle builds S explicitly (d·κs nonzeros in float64 CSR): beyond 2^28 nonzeros it does
+    # not fit the host, so no bounded sample of this workload exists for it
+    return cfg.d * cfg.kappa * cfg.s <= (1 << 28)
 
 
 def reference_arm(args, cfg, rank):
+    """--impl reference: the oracle (there is no reference implementation to install,
+    DESIGN.md §8), as it stands, on the host cores; every step = S build + pooled product on a
+    bounded column sample.  Rank 0 only; other ranks exit without work."""
     if rank != 0:
         return
-    import numpy as np
-
-    n_s = max(1, min(cfg.n, 32))
-    # each step = the oracle on a bounded n_s-column sample of the config
-    import oracle
-    import synth
-
-    osk = oracle.make_sketch(cfg.M, cfg.B_r, cfg.B_c, cfg.kappa, cfg.s, cfg.seed)
-    A = synth.host_matrix("gaussian", cfg.d, n_s, seed=3, dtype=np.float32)
-    for _ in range(args.warmup):
-        oracle.apply(osk, A)
+    if not oracle_fits(cfg):
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle cannot build S for {cfg.name} "
+                          f"(d*kappa*s = {cfg.d * cfg.kappa * cfg.s} > 2^28 nonzeros)"}), flush=True)
+        return
+    n_s = max(1, min(cfg.n, args.ref_cols))
+    oracle_timing(cfg, n_s, repeats=max(1, min(args.warmup, 1)))  # warm-up (imports, page-in)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.apply(osk, A)
+    tm = oracle_timing(cfg, n_s, repeats=args.steps)
     dt = (time.perf_counter() - t0) / args.steps
     gbs = cfg.roofline_bytes(n_s) / dt / 1e9
-    sample = f"{n_s} of {cfg.n} columns of the {cfg.name} config per step (S built + multiplied in float64)"
+    sample = (f"{n_s} of {cfg.n} columns of {cfg.name} per step: S built in float64 CSR "
+              f"(median {tm['build_s']:.2f} s) + product over {tm['cores']} worker processes "
+              f"(median {tm['multiply_s']:.2f} s)")
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
@@ -172,17 +209,65 @@ def reference_arm(args, cfg, rank):
         "config": {"workload": cfg.name, "d": cfg.d, "k": cfg.k, "kappa": cfg.kappa, "s": cfg.s, "n": n_s,
                    "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c},
         "columns_per_s": n_s / dt,
-        "cpu_baseline": {"value": gbs, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": gbs, "unit": UNIT, "cores": tm["cores"], "kind": "oracle", "sample": sample,
+                         "build_s": tm["build_s"], "multiply_s": tm["multiply_s"]},
         "e2e": {"value": gbs, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def relaunch(args):
+    """--gpus N without a torchrun environment: re-exec this script under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1); rank 0 prints the line."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def dry_run(args, world, rank):
+    """--dry-run: the launcher / aggregation path without a GPU (gloo; a numpy step stands in for the
+    apply).  Used by the CPU tests of the multi-process plumbing."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    x = np.random.default_rng(rank).standard_normal((256, 256))
+    for _ in range(max(3, args.warmup)):
+        x = np.tanh(x @ x.T / 256)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x = np.tanh(x @ x.T / 256)
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        ms = float(t.item()) / args.steps * 1e3
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms, "dry_run": True,
+                          "comm": {"backend": "gloo", "world": world}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))  # one process per GPU under torch.distributed.run
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry_run:
+        dry_run(args, world, rank)
+        return
     from paper_2602_06071_b200 import configs as C
 
     cfg = C.CONFIGS[args.config]
@@ -198,8 +283,15 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    comm = None
     if world > 1:
+        # NCCL prints its communicator init (nranks, NVLink/NVLS topology) to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
+        one = torch.ones(1, device=dev)
+        dist.all_reduce(one)
+        comm = {"backend": dist.get_backend(), "world": dist.get_world_size(), "allreduce_of_ones": float(one.item())}
     n = cfg.n
     tdt = torch.float32 if cfg.dtype == "f32" else torch.bfloat16
     sk = Sketch(**cfg.sketch_args(), kind=args.sketch, **({"mode": args.mode} if args.sketch == "blockperm" else {}))
@@ -277,6 +369,25 @@ def main():
         ev[i + 1].record(stream)
     torch.cuda.synchronize(dev)
     launches = lib.bps_kernel_launches() - l0
+    # the dominant kernel's mean launch time: CUDA events the library records on the launch stream
+    # around it, in a second run of the same steps (events between the stream kernel and the
+    # combine pass would serialise their programmatic dependent launch, so not in the timed region)
+    kern_ms = aux_ms = None
+    timing = hasattr(lib, "bps_timing_enable")
+    if timing:
+        import ctypes
+
+        lib.bps_timing_enable(1)
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize(dev)
+        lib.bps_timing_enable(0)
+        tot, cnt = ctypes.c_double(), ctypes.c_uint64()
+        if lib.bps_timing_read(ctypes.byref(tot), ctypes.byref(cnt)) == 0 and cnt.value:
+            kern_ms = tot.value / cnt.value
+            launches_main = cnt.value
+        if lib.bps_timing_read_ex(1, ctypes.byref(tot), ctypes.byref(cnt)) == 0 and cnt.value:
+            aux_ms = tot.value / args.steps
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -295,7 +406,42 @@ def main():
         bytes_rank = cfg.k * n * (cfg.kappa * cfg.s * cfg.elem + 4)
     value = world * bytes_rank / (ms / 1e3) / 1e9
     peak, peak_src = measured_peaks()
-    achieved = bytes_rank / (statistics.mean(per) / 1e3) / 1e9
+    # roofline of the dominant kernel: algorithmic bytes per launch / its mean launch duration
+    launches_per_step = (launches_main / args.steps) if kern_ms else None
+    if kern_ms and launches_per_step and launches_per_step > 1:  # scale-out panels: several launches per step
+        achieved = (bytes_rank / launches_per_step) / (kern_ms / 1e3) / 1e9
+    else:
+        achieved = bytes_rank / ((kern_ms if kern_ms else statistics.mean(per)) / 1e3) / 1e9
+
+    # strong scaling (column mode, N > 1): the config's n columns split over the ranks (tile-aligned,
+    # dist.column_shard), max-over-ranks device time, value = the whole job's bytes / that time
+    strong = None
+    if world > 1 and args.shard == "column" and not args.no_strong and args.op == "apply" and args.layout == "n" \
+            and cfg.name != "scaleout":
+        from paper_2602_06071_b200 import dist as D
+
+        c0, c1 = D.column_shard(cfg.n, world, rank, align=128)
+        A_s, Y_s = A[:, c0:c1], Y[:, c0:c1]
+
+        def sstep():
+            if c1 > c0:
+                sk.apply(A_s, out=Y_s, variant=args.variant, use_workspace=not args.no_workspace)
+
+        for _ in range(max(3, args.warmup)):
+            sstep()
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            sstep()
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        ts = torch.tensor([s0.elapsed_time(s1) / args.steps], device=dev, dtype=torch.float64)
+        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        strong = {"value": cfg.roofline_bytes(cfg.n) / (float(ts.item()) / 1e3) / 1e9, "unit": UNIT,
+                  "ms_per_step": float(ts.item()), "n_total": cfg.n, "n_per_rank_max": -(-cfg.n // 128 // world) * 128,
+                  "scaling": "strong", "shard": "dist.column_shard (128-column aligned)"}
 
     # end-to-end through the public API with pinned host buffers (H2D + apply + D2H per step)
     e2e = None
@@ -334,16 +480,16 @@ def main():
         del A_h, Y_h
 
     cpu = None
-    if cfg.d * cfg.kappa * cfg.s > (1 << 28):
-        # the oracle builds S explicitly (d·κs nonzeros in float64 CSR): beyond 2^28 nonzeros it does
-        # not fit the host, so no bounded sample of this workload exists for it
+    if not oracle_fits(cfg):
         args.no_cpu_baseline = True
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_s = min(cfg.n, 64)
-        t_cpu, b_cpu, reps = cpu_baseline(cfg, n_s)
-        cpu = {"value": b_cpu / t_cpu / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{n_s} of {cfg.n} columns of {cfg.name}, float64 S build + CSR multiply, median of {reps} "
-                         f"({t_cpu:.2f} s each); numpy/scipy single-threaded",
+        n_s = min(cfg.n, 256)
+        tm = oracle_timing(cfg, n_s, repeats=2)
+        t_cpu = tm["build_s"] + tm["multiply_s"]
+        cpu = {"value": cfg.roofline_bytes(n_s) / t_cpu / 1e9, "unit": UNIT, "cores": tm["cores"], "kind": "oracle",
+               "sample": f"{n_s} of {cfg.n} columns of {cfg.name}: S built in float64 CSR (median {tm['build_s']:.2f} s, "
+                         f"one core) + product over {tm['cores']} worker processes (median {tm['multiply_s']:.2f} s)",
+               "build_s": tm["build_s"], "multiply_s": tm["multiply_s"],
                "host_cores_available": len(os.sched_getaffinity(0))}
 
     if rank == 0:
@@ -368,8 +514,13 @@ def main():
                          "traffic": ncu_traffic(cfg.name + (":t" if args.layout == "t" else "") + (":affine" if args.mode == "affine" else ""),
                                                 args.variant) if (args.op == "apply" and args.sketch == "blockperm") else None,
                          "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": bytes_rank},
+                         "kernel": "bps_tc_kernel" if args.variant != "sparse" else "sparse gather kernel",
+                         "kernel_ms_mean": kern_ms,
+                         "aux_ms_per_step": aux_ms if timing else None,
+                         "algorithmic_bytes_per_launch": bytes_rank / (launches_per_step or 1)},
             "gpu_launches": launches,
+            **({"strong_scaling": strong} if strong else {}),
+            **({"comm": comm} if comm else {}),
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -248,6 +248,16 @@ int bps_pattern_host(const bps_sketch* sk, int64_t g, int32_t ell, int64_t u, in
  * many of the library's own kernels ran inside a timed region. */
 uint64_t bps_kernel_launches(void);
 
+/* Live timing of the dominant kernel (the bench's roofline figure): after bps_timing_enable(1),
+ * every apply records a CUDA-event pair on its stream around its main kernel (tc stream kernel or
+ * sparse gather kernel, not the combine pass); bps_timing_read synchronises on them, returns the
+ * summed milliseconds and the number of launches, and clears the record.  Host-side state is
+ * process-global and mutex-protected. */
+int bps_timing_enable(int on);
+int bps_timing_read(double* total_ms, uint64_t* count);
+/* aux = 1: the same for the auxiliary kernels (the tc combine pass); aux = 0 is bps_timing_read. */
+int bps_timing_read_ex(int aux, double* total_ms, uint64_t* count);
+
 /* Library / build information ("bps <version> sm_100a ..."). */
 const char* bps_version(void);
 

@@ -9,11 +9,23 @@ is missing or the device is not sm_100, calls raise.
     sk = Sketch(M=128, B_r=32, B_c=8192, kappa=4, s=4, seed=1234)
     Y = sk.apply(A)            # A: cuda tensor d×n (float32 or bfloat16) -> Y: k×n float32
     Yt = sk.apply_t(X)         # X: n×d -> Yt: n×k
+
+The library is loaded on first use of ``Sketch``/``lib`` (not by importing submodules such as
+``configs``), so host-only tools — the bench's CPU-oracle arm — never map it.
 """
 
 from __future__ import annotations
 
-from ._lib import BpsError, lib, lib_path  # noqa: F401
-from .sketch import VARIANTS, Sketch  # noqa: F401
-
 __all__ = ["Sketch", "BpsError", "VARIANTS", "lib", "lib_path"]
+
+
+def __getattr__(name):
+    if name in ("BpsError", "lib", "lib_path"):
+        from . import _lib
+
+        return getattr(_lib, name)
+    if name in ("Sketch", "VARIANTS"):
+        from . import sketch
+
+        return getattr(sketch, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -9,6 +9,8 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "bps_internal.h"
 
@@ -18,6 +20,28 @@ static thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+// ---- live timing of the dominant kernel (bps_timing_enable / bps_timing_read)
+static std::mutex g_tmu;
+static bool g_timing = false;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_tev, g_tev_aux;
+bool timing_begin(cudaStream_t st, cudaEvent_t ev[2]) {
+  {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    if (!g_timing) return false;
+  }
+  if (cudaEventCreate(&ev[0]) != cudaSuccess || cudaEventCreate(&ev[1]) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaEventRecord(ev[0], st);
+  return true;
+}
+void timing_end(cudaStream_t st, cudaEvent_t ev[2], bool aux) {
+  cudaEventRecord(ev[1], st);
+  std::lock_guard<std::mutex> lk(g_tmu);
+  (aux ? g_tev_aux : g_tev).emplace_back(ev[0], ev[1]);
+}
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
@@ -142,6 +166,37 @@ extern "C" {
 const char* bps_last_error(void) { return g_last_error.c_str(); }
 
 uint64_t bps_kernel_launches(void) { return g_launches.load(); }
+
+int bps_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_timing = on != 0;
+  return BPS_OK;
+}
+
+int bps_timing_read_ex(int aux, double* total_ms, uint64_t* count) {
+  if (!total_ms || !count) return fail(BPS_ERR_INVALID_ARG, "NULL argument");
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+  {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    evs.swap(aux ? g_tev_aux : g_tev);
+  }
+  double tot = 0;
+  int rc = BPS_OK;
+  for (auto& pr : evs) {
+    float ms = 0;
+    cudaError_t e = cudaEventSynchronize(pr.second);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, pr.first, pr.second);
+    if (e != cudaSuccess) rc = fail(BPS_ERR_CUDA, std::string("bps_timing_read: ") + cudaGetErrorString(e));
+    tot += ms;
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  *total_ms = tot;
+  *count = evs.size();
+  return rc;
+}
+
+int bps_timing_read(double* total_ms, uint64_t* count) { return bps_timing_read_ex(0, total_ms, count); }
 
 const char* bps_version(void) { return "bps 0.1 sm_100a (sparse gather + tcgen05 NT band kernel)"; }
 

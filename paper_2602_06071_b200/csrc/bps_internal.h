@@ -21,6 +21,9 @@ struct bps_sketch {
 namespace bps {
 
 extern std::atomic<uint64_t> g_launches;
+// bps_timing_enable: CUDA events around the dominant kernel of every apply (bps_api.cu)
+bool timing_begin(cudaStream_t st, cudaEvent_t ev[2]);
+void timing_end(cudaStream_t st, cudaEvent_t ev[2], bool aux = false);
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 

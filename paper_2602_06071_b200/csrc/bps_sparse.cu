@@ -266,6 +266,8 @@ int launch_sparse_rowmajor(const SketchParams& p, const void* A, int64_t lda, in
   const int64_t ntiles = (n + TN - 1) / TN;
   if (ntiles > 65535) return fail(BPS_ERR_UNSUPPORTED, "sparse kernel: n too large for grid.y");
   dim3 grid((unsigned)pl.n_out, (unsigned)ntiles), block(32 * W);
+  cudaEvent_t tev[2] = {nullptr, nullptr};
+  const bool timed = timing_begin(st, tev);
   if (dt == BPS_F32) {
     cudaFuncSetAttribute(sparse_rowmajor_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     sparse_rowmajor_kernel<float><<<grid, block, smem, st>>>(p, (const float*)A, lda, n, Y, ldy, pl.range_mode,
@@ -275,6 +277,7 @@ int launch_sparse_rowmajor(const SketchParams& p, const void* A, int64_t lda, in
     sparse_rowmajor_kernel<__nv_bfloat16><<<grid, block, smem, st>>>(p, (const __nv_bfloat16*)A, lda, n, Y, ldy,
                                                                      pl.range_mode, pl.pos_begin);
   }
+  if (timed) timing_end(st, tev);
   return launch_err("sparse_rowmajor_kernel");
 }
 
@@ -285,6 +288,8 @@ int launch_sparse_transposed(const SketchParams& p, const void* X, int64_t ldx, 
   const int64_t ntiles = (n + 127) / 128;
   if (ntiles > 65535) return fail(BPS_ERR_UNSUPPORTED, "sparse kernel: n too large for grid.y");
   dim3 grid((unsigned)pl.n_out, (unsigned)ntiles), block(256);
+  cudaEvent_t tev[2] = {nullptr, nullptr};
+  const bool timed = timing_begin(st, tev);
   if (dt == BPS_F32) {
     cudaFuncSetAttribute(sparse_transposed_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     sparse_transposed_kernel<float><<<grid, block, smem, st>>>(p, (const float*)X, ldx, n, Yt, ldyt, pl.range_mode,
@@ -295,6 +300,7 @@ int launch_sparse_transposed(const SketchParams& p, const void* X, int64_t ldx, 
     sparse_transposed_kernel<__nv_bfloat16><<<grid, block, smem, st>>>(p, (const __nv_bfloat16*)X, ldx, n, Yt, ldyt,
                                                                        pl.range_mode, pl.pos_begin);
   }
+  if (timed) timing_end(st, tev);
   return launch_err("sparse_transposed_kernel");
 }
 

@@ -52,6 +52,7 @@ namespace tcx {
 namespace {
 
 constexpr int kBandTile = 128 * kBK * 2;  // one M-tile (128 band rows) of a band stage, bytes
+constexpr int kMaxRanges = 511;           // canon: stream ranges per column tile (TcArgs::rb)
 
 // Warp roles (the issue arbiter favours high warp ids, so the latency-critical single-thread
 // roles take the last two warps): 0-3 epilogue (TMEM lane quarters 0-3) | 4-11 band
@@ -149,6 +150,8 @@ struct TcArgs {
   int64_t stream_begin;        // first input position of the launch window
   int64_t stream_len;          // number of input positions in the window
   int R;                       // ranges per column tile
+  // canon: first stage of range r, r = 0..R (host-computed G·⌊NGt·r/R⌋: no 64-bit divisions on the device)
+  int rb[kMaxRanges + 1];
   int nct;                     // column tiles (multiple of the cluster size); CTA = (range, tile)
   int canon;                   // 1: stream ranges + owner/contributor workspace; 0: halo ranges
   int64_t n_out;               // halo: outputs of the launch window; output o is position i_first + o
@@ -162,7 +165,7 @@ struct TcArgs {
   uint32_t mma_hint;           // MMA issuer's mbarrier suspend-time hint (ns)
   int ab;                      // A/B knob (env BPS_TC_AB): 2 skip contributor tile writes (results
                                // wrong), 4 evict_normal for partials, 8 combine with 128 threads,
-                               // 16 combine without programmatic dependent launch
+                               // 16 combine without programmatic dependent launch, 32 skip the main kernel
   int dbg;  // experiment switches (env BPS_TC_DEBUG; 0 in production): 1 no band, 2 no convert, 4 no MMA,
             // 8 cycle trace, 16 no band proxy fence, 32 band without hashing
   unsigned long long* trace;   // dbg & 8: per-CTA cycle counters (16 per CTA), else nullptr
@@ -177,19 +180,22 @@ struct CanonGeom {
   // fields copied by value: holding a reference to the kernel's parameter struct would force it
   // into local memory (its address escapes) and every args access through L1
   float* W;
+  const int* rb;  // TcArgs::rb (kernel parameter space)
   int64_t tpc, NGt;
   int nct, nk, bn, G, R, slen, sb, kap, npg, Ts, KN, Br;
   __device__ __forceinline__ CanonGeom(const TcArgs& a, int nk_, int bn_) : nk(nk_), bn(bn_) {
-    W = a.W, tpc = a.tpc, nct = a.nct;
+    W = a.W, tpc = a.tpc, nct = a.nct, rb = a.rb;
     G = a.G, R = a.R, slen = (int)a.stream_len, sb = (int)a.stream_begin, kap = (int)a.p.kappa;
     npg = nk / G, Ts = slen * nk, KN = kap * nk, Br = (int)a.p.B_r, NGt = (int64_t)a.stream_len * nk / G;
   }
-  __device__ int range_begin(int r) const { return G * (int)(NGt * r / R); }
-  __device__ int range_of(int x) const {  // range holding stream stage x ∈ [0, Ts)
-    int r = (int)((int64_t)(x / G) * R / NGt);
-    while (r + 1 < R && range_begin(r + 1) <= x) ++r;
-    while (r > 0 && range_begin(r) > x) --r;
-    return r;
+  __device__ int range_begin(int r) const { return rb[r]; }
+  __device__ int range_of(int x) const {  // range holding stream stage x ∈ [0, Ts): binary search
+    int lo = 0, hi = R;  // rb[lo] ≤ x < rb[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (rb[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
   }
   __device__ int first_stage(int i) const { return (i + 1 - sb) * nk; }
   // partial tile of (range r, column tile ct, straddler j, group lg of the range): TF tiles are
@@ -368,8 +374,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
   const int64_t NGt = args.stream_len * nk / G;  // canon: groups in the stream
   if (args.canon) {
     sb = args.stream_begin;
-    S0 = (int64_t)G * (NGt * rr / args.R);
-    S1 = (int64_t)G * (NGt * (rr + 1) / args.R);
+    S0 = args.rb[rr];
+    S1 = args.rb[rr + 1];
   } else {
     const int64_t o0 = args.n_out * rr / args.R, o1 = args.n_out * (rr + 1) / args.R;
     ilo = args.i_first + o0;
@@ -1347,7 +1353,11 @@ __global__ void __launch_bounds__(256) bps_tc_combine(const __grid_constant__ Tc
   const SketchParams& p = args.p;
   const int nk = (int)(p.B_c / kBK);
   const CanonGeom geo(args, nk, BN);
+  // blockIdx.x = (output o, column tile ct, element part): each CTA takes 1/nsplit of the tile's
+  // elements, at most EPT per thread, so that all of them are in flight in one pass
+  const unsigned nsplit = gridDim.y;
   const int ct = (int)(blockIdx.x % (unsigned)args.nct), o = (int)(blockIdx.x / (unsigned)args.nct);
+  const int part = (int)blockIdx.y;
   const int i = (int)args.i_first + o;  // owner coordinates (first stage o·nk ≥ 0)
   const int F = geo.first_stage(i);
   if (F + geo.KN <= geo.range_begin(geo.range_of(F) + 1)) return;  // finished by its owner
@@ -1363,12 +1373,13 @@ __global__ void __launch_bounds__(256) bps_tc_combine(const __grid_constant__ Tc
   // programmatic dependent launch: everything above ran while bps_tc_kernel was finishing; its
   // prefixes and partial tiles are visible after this wait
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int nt = ntiles, NT = (int)blockDim.x, Br = geo.Br, nel = Br * BN;
+  const int nt = ntiles, NT = (int)blockDim.x, Br = geo.Br;
+  const int el0 = (int)((int64_t)Br * BN * part / nsplit), nel = (int)((int64_t)Br * BN * (part + 1) / nsplit);
   const int64_t col0 = (int64_t)ct * BN;
   const int64_t yr0 = args.range_mode ? (int64_t)(i - args.pos_begin) * Br : (int64_t)affine_pow(p, (uint64_t)i, 0u) * Br;
   float* const Yb = TRANS ? args.Y + col0 * args.ldy + yr0 : args.Y + yr0 * args.ldy + col0;
   bool bad = false;
-  for (int e0 = (int)threadIdx.x; e0 < nel; e0 += EPT * NT) {
+  for (int e0 = el0 + (int)threadIdx.x; e0 < nel; e0 += EPT * NT) {
     int off[EPT];      // element offset inside a tile (TF: row-major [B_r][BN]; else [BN][B_r])
     int64_t yo[EPT];   // element offset from Yb, or -1
     float acc[EPT];
@@ -1381,7 +1392,7 @@ __global__ void __launch_bounds__(256) bps_tc_combine(const __grid_constant__ Tc
       yo[k] = ok ? (TRANS ? (int64_t)c * args.ldy + r : (int64_t)r * args.ldy + c) : -1;
     }
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) acc[k] = yo[k] >= 0 ? ld_cg_f(Yb + yo[k]) : 0.f;
+    for (int k = 0; k < EPT; ++k) acc[k] = yo[k] >= 0 ? __ldcg(Yb + yo[k]) : 0.f;
     // canonical order: acc = ((prefix + P_1) + P_2) + …; the loads of TB tiles are issued together
     for (int t0 = 0; t0 < nt; t0 += TB) {
       float v[TB * EPT];
@@ -1389,7 +1400,7 @@ __global__ void __launch_bounds__(256) bps_tc_combine(const __grid_constant__ Tc
       for (int b = 0; b < TB; ++b) {
         const float* tp = tiles[min(t0 + b, nt - 1)];
 #pragma unroll
-        for (int k = 0; k < EPT; ++k) v[b * EPT + k] = ld_cg_f(tp + off[k]);
+        for (int k = 0; k < EPT; ++k) v[b * EPT + k] = (t0 + b < nt) ? __ldcg(tp + off[k]) : 0.f;
       }
 #pragma unroll
       for (int b = 0; b < TB; ++b)
@@ -1538,8 +1549,13 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     const int64_t r = atoll(e);
     if (r >= 1 && r <= R) R = r;
   }
+  if (a.canon && R > kMaxRanges) R = kMaxRanges;
   a.R = (int)R;
   a.nct = (int)n_ct;
+  if (a.canon) {
+    const int64_t NGt = a.stream_len * nk / hp.G;
+    for (int64_t r = 0; r <= R; ++r) a.rb[r] = (int)(hp.G * (NGt * r / R));
+  }
   const int64_t grid = n_ct * R;
   if (grid > 0x7FFFFFFF) return fail(BPS_ERR_UNSUPPORTED, "grid too large");
 
@@ -1615,7 +1631,10 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     cudaFree(a.trace);
   }
 #else
-  e = launch();
+  cudaEvent_t tev[2] = {nullptr, nullptr};
+  const bool timed = timing_begin(st, tev);
+  e = (a.ab & 32) ? cudaSuccess : launch();  // ab & 32: combine only (timing experiment)
+  if (timed) timing_end(st, tev);
   g_launches.fetch_add(1, std::memory_order_relaxed);
 #endif
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -1625,15 +1644,20 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     const int64_t cgrid = n_ct * pl.n_out;
     if (cgrid > 0x7FFFFFFF) return fail(BPS_ERR_UNSUPPORTED, "combine grid too large");
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)cgrid);
-    cfg.blockDim = dim3((a.ab & 8) ? 128 : 256);
+    const int cthreads = (a.ab & 8) ? 128 : 256;
+    const int nsplit = (int)std::max<int64_t>(1, ((int64_t)p.B_r * BN + cthreads * 4 - 1) / (cthreads * 4));
+    cfg.gridDim = dim3((unsigned)cgrid, (unsigned)std::min(nsplit, 65535));
+    cfg.blockDim = dim3(cthreads);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = (a.ab & 16) ? 0 : 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    cudaEvent_t cev[2] = {nullptr, nullptr};
+    const bool ctimed = timing_begin(st, cev);
     e = cudaLaunchKernelEx(&cfg, bps_tc_combine<F32, TRANS, BN, TF>, a);
+    if (ctimed) timing_end(st, cev, true);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("bps_tc_combine launch: ") + cudaGetErrorString(e));
