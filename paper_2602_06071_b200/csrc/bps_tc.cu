@@ -38,10 +38,20 @@ namespace {
 struct Coverage {
   bool ok = false;
   int nmt = 1;
+  int ss = 1;  // slot split (row-major, κ·B_r in (128, 512]): SS CTAs of a cluster share the data
   std::string why;
 };
 
-Coverage coverage(const SketchParams& p, bps_dtype dt) {
+// Slot split applies to the row-major layout when the κ band slots divide into SS = 2 or 4
+// groups of ≤ 128 band rows (one M-tile per CTA); disable with BPS_TC_NOSS=1 (A/B knob).
+int slot_split(const SketchParams& p, bool transposed) {
+  const uint64_t rows = (uint64_t)p.kappa * p.B_r;
+  if (transposed || rows <= 128 || rows > 512 || getenv("BPS_TC_NOSS")) return 1;
+  const int ss = rows <= 256 ? 2 : 4;
+  return (p.kappa % ss == 0 && (uint64_t)(p.kappa / ss) * p.B_r <= 128) ? ss : 1;
+}
+
+Coverage coverage(const SketchParams& p, bps_dtype dt, bool transposed) {
   Coverage c;
   if (dt != BPS_F32 && dt != BPS_BF16) {
     c.why = "dtype";
@@ -52,8 +62,9 @@ Coverage coverage(const SketchParams& p, bps_dtype dt) {
     return c;
   }
   const uint64_t rows = (uint64_t)p.kappa * p.B_r;
-  if (rows > 512 || (rows > 256 && dt != BPS_BF16)) {
-    c.why = "tc variant needs kappa*B_r <= 256 (fp32) or <= 512 (bf16)";
+  c.ss = slot_split(p, transposed);
+  if (rows > 512 || (rows > 256 && dt != BPS_BF16 && c.ss == 1)) {
+    c.why = "tc variant needs kappa*B_r <= 256 (fp32) or <= 512 (bf16, or fp32 row-major with kappa % 4 == 0)";
     return c;
   }
   if ((uint64_t)p.kappa * p.s > 128) {
@@ -62,11 +73,11 @@ Coverage coverage(const SketchParams& p, bps_dtype dt) {
   }
   // more than 2 band tiles: rows ≥ 256 need the row-partitioned fast/dense generators (16-bit
   // stale-entry offsets), i.e. C = B_r/s a power of two and κs a multiple of 4
-  if (rows > 256 && p.mode == 0 && ((p.C & (p.C - 1)) != 0 || ((uint64_t)p.kappa * p.s) % 4 != 0)) {
+  if (rows > 256 && c.ss == 1 && p.mode == 0 && ((p.C & (p.C - 1)) != 0 || ((uint64_t)p.kappa * p.s) % 4 != 0)) {
     c.why = "tc variant with kappa*B_r > 256 needs B_r/s a power of two and kappa*s % 4 == 0";
     return c;
   }
-  c.nmt = rows <= 128 ? 1 : (rows <= 256 ? 2 : 4);
+  c.nmt = c.ss > 1 ? 1 : (rows <= 128 ? 1 : (rows <= 256 ? 2 : 4));
   c.ok = true;
   return c;
 }
@@ -99,15 +110,30 @@ int device_sms() {
 
 struct Choice {
   bool f32, trans, tf, rl;
-  int nmt, bn, cs;
+  int nmt, bn, cs, ss;
 };
 
-Choice choose(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl, int nmt, int sms,
-              bool canon, int G) {
+Choice choose(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl, int nmt, int ss,
+              int sms, bool canon, int G) {
   Choice c{};
   c.f32 = dt == BPS_F32;
   c.trans = transposed;
   c.nmt = nmt;
+  c.ss = ss;
+  if (ss > 1) {  // slot split: one band tile per CTA, NT form, no band sharing across column tiles
+    c.tf = c.rl = false;
+    c.cs = 1;
+    if (c.f32) {
+      c.bn = 128;
+    } else {
+      const int64_t ct256 = (n + 255) / 256, ct128 = (n + 127) / 128, cl = std::max(1, sms / ss);
+      const int64_t used256 = ct256 >= cl ? ct256 : ct256 * (cl / ct256);
+      const int64_t used128 = ct128 >= cl ? ct128 : ct128 * (cl / ct128);
+      c.bn = (used256 * 10 >= used128 * 9 || used256 >= cl) ? 256 : 128;
+      if (const char* e = getenv("BPS_TC_BN")) c.bn = atoi(e) == 128 ? 128 : 256;  // tuning knob
+    }
+    return c;
+  }
   const int64_t n_out = pl.range_mode ? pl.n_out : (int64_t)p.M;
   (void)n_out;
   if (c.f32) {
@@ -143,7 +169,7 @@ Choice choose(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, c
 
 int supported_impl(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl) {
   (void)transposed;
-  Coverage cv = coverage(p, dt);
+  Coverage cv = coverage(p, dt, transposed);
   if (!cv.ok) return fail(BPS_ERR_UNSUPPORTED, cv.why);
   const int64_t in_rows = (pl.range_mode ? pl.n_out + (int64_t)p.kappa - 1 : (int64_t)p.M) * (int64_t)p.B_c;
   if (in_rows > 0x7FFFFFFF || n > 0x7FFFFFFF)
@@ -152,11 +178,11 @@ int supported_impl(const SketchParams& p, int64_t n, bps_dtype dt, bool transpos
 }
 
 size_t workspace_impl(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, const Placement& pl) {
-  Coverage cv = coverage(p, dt);
+  Coverage cv = coverage(p, dt, transposed);
   if (!cv.ok || n <= 0) return 0;
   const int sms = device_sms();
   const int G = group_for(p);
-  const Choice c = choose(p, n, dt, transposed, pl, cv.nmt, sms, true, G);
+  const Choice c = choose(p, n, dt, transposed, pl, cv.nmt, cv.ss, sms, true, G);
   const int64_t nct = (n + c.bn - 1) / c.bn;
   const int64_t ctas = std::max<int64_t>(nct, sms);  // grid = nct·R ≤ max(nct, co-resident slots)
   return (size_t)ctas * (size_t)tiles_per_cta(p, G) * p.B_r * c.bn * 4;
@@ -164,7 +190,7 @@ size_t workspace_impl(const SketchParams& p, int64_t n, bps_dtype dt, bool trans
 
 int launch_tc_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt, float* Y, int64_t ldy,
               bool transposed, const Placement& pl, void* ws, size_t ws_bytes, cudaStream_t st) {
-  Coverage cv = coverage(p, dt);
+  Coverage cv = coverage(p, dt, transposed);
   if (!cv.ok) return fail(BPS_ERR_UNSUPPORTED, cv.why);
   HostPlan hp{};
   hp.sms = device_sms();
@@ -175,10 +201,11 @@ int launch_tc_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n,
              (int64_t)p.kappa * ((p.B_c / kBK) / hp.G) <= 1024;
   hp.ws = hp.canon ? ws : nullptr;
   hp.ws_bytes = hp.canon ? ws_bytes : 0;
-  const Choice c = choose(p, n, dt, transposed, pl, cv.nmt, hp.sms, hp.canon, hp.G);
-#define BPS_TC_MATCH(F, T, NM, B, C, TF_, RL_)                                                                \
-  if (c.f32 == F && c.trans == T && c.nmt == NM && c.bn == B && c.cs == C && c.tf == TF_ && c.rl == RL_) \
-    return launch_impl<F, T, NM, B, C, TF_, RL_>(p, A, lda, n, Y, ldy, pl, hp, st);
+  const Choice c = choose(p, n, dt, transposed, pl, cv.nmt, cv.ss, hp.sms, hp.canon, hp.G);
+#define BPS_TC_MATCH(F, T, NM, B, C, TF_, RL_, SS_)                                                       \
+  if (c.f32 == F && c.trans == T && c.nmt == NM && c.bn == B && c.cs == C && c.tf == TF_ && c.rl == RL_ && \
+      c.ss == SS_)                                                                                        \
+    return launch_impl<F, T, NM, B, C, TF_, RL_, SS_>(p, A, lda, n, Y, ldy, pl, hp, st);
   BPS_TC_INSTANTIATIONS(BPS_TC_MATCH)
 #undef BPS_TC_MATCH
   return fail(BPS_ERR_UNSUPPORTED, "no tc instantiation for this plan");

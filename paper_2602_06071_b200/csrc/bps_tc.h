@@ -24,43 +24,49 @@ struct HostPlan {
 
 // One tcgen05 kernel configuration (template arguments of bps_tc_kernel).
 #define BPS_TC_INSTANTIATIONS(X)                                                                  \
-  X(true, false, 1, 128, 1, true, false)   /* fp32 row-major, T form (data in TMEM)           */ \
-  X(true, false, 1, 128, 2, true, false)                                                          \
-  X(true, true, 1, 128, 1, false, false)   /* fp32 transposed, one band tile                   */ \
-  X(true, true, 1, 128, 2, false, false)                                                          \
-  X(true, false, 2, 64, 1, false, false)   /* fp32, κ·B_r in (128, 256]                        */ \
-  X(true, false, 2, 64, 2, false, false)                                                          \
-  X(true, true, 2, 64, 1, false, false)                                                           \
-  X(true, true, 2, 64, 2, false, false)                                                           \
-  X(false, false, 1, 256, 1, false, false) /* bf16 row-major                                    */ \
-  X(false, false, 1, 256, 2, false, false)                                                        \
-  X(false, false, 1, 128, 1, false, false)                                                        \
-  X(false, false, 1, 128, 2, false, false)                                                        \
-  X(false, false, 1, 64, 1, false, false)  /* narrow n                                          */ \
-  X(false, false, 1, 64, 2, false, false)                                                         \
-  X(false, true, 1, 256, 1, false, true)   /* bf16 transposed: K-pair boxes + re-layout         */ \
-  X(false, true, 1, 256, 2, false, true)                                                          \
-  X(false, true, 1, 128, 1, false, true)                                                          \
-  X(false, true, 1, 128, 2, false, true)                                                          \
-  X(false, true, 1, 256, 1, false, false)  /* bf16 transposed, plain SW128 boxes (B_c % 128)    */ \
-  X(false, true, 1, 256, 2, false, false)                                                         \
-  X(false, true, 1, 128, 1, false, false)                                                         \
-  X(false, true, 1, 128, 2, false, false)                                                         \
-  X(false, false, 2, 128, 1, false, false) /* bf16, κ·B_r in (128, 256]                        */ \
-  X(false, false, 2, 128, 2, false, false)                                                        \
-  X(false, true, 2, 128, 1, false, false)                                                         \
-  X(false, true, 2, 128, 2, false, false)                                                         \
-  X(false, false, 4, 64, 1, false, false)  /* bf16, κ·B_r in (256, 512]                        */ \
-  X(false, false, 4, 64, 2, false, false)                                                         \
-  X(false, true, 4, 64, 1, false, false)                                                          \
-  X(false, true, 4, 64, 2, false, false)
+  X(true, false, 1, 128, 1, true, false, 1)   /* fp32 row-major, T form (data in TMEM)           */ \
+  X(true, false, 1, 128, 2, true, false, 1)                                                          \
+  X(true, true, 1, 128, 1, false, false, 1)   /* fp32 transposed, one band tile                   */ \
+  X(true, true, 1, 128, 2, false, false, 1)                                                          \
+  X(true, false, 2, 64, 1, false, false, 1)   /* fp32, κ·B_r in (128, 256]                        */ \
+  X(true, false, 2, 64, 2, false, false, 1)                                                          \
+  X(true, true, 2, 64, 1, false, false, 1)                                                           \
+  X(true, true, 2, 64, 2, false, false, 1)                                                           \
+  X(false, false, 1, 256, 1, false, false, 1) /* bf16 row-major                                    */ \
+  X(false, false, 1, 256, 2, false, false, 1)                                                        \
+  X(false, false, 1, 128, 1, false, false, 1)                                                        \
+  X(false, false, 1, 128, 2, false, false, 1)                                                        \
+  X(false, false, 1, 64, 1, false, false, 1)  /* narrow n                                          */ \
+  X(false, false, 1, 64, 2, false, false, 1)                                                         \
+  X(false, true, 1, 256, 1, false, true, 1)   /* bf16 transposed: K-pair boxes + re-layout         */ \
+  X(false, true, 1, 256, 2, false, true, 1)                                                          \
+  X(false, true, 1, 128, 1, false, true, 1)                                                          \
+  X(false, true, 1, 128, 2, false, true, 1)                                                          \
+  X(false, true, 1, 256, 1, false, false, 1)  /* bf16 transposed, plain SW128 boxes (B_c % 128)    */ \
+  X(false, true, 1, 256, 2, false, false, 1)                                                         \
+  X(false, true, 1, 128, 1, false, false, 1)                                                         \
+  X(false, true, 1, 128, 2, false, false, 1)                                                         \
+  X(false, false, 2, 128, 1, false, false, 1) /* bf16, κ·B_r in (128, 256]                        */ \
+  X(false, false, 2, 128, 2, false, false, 1)                                                        \
+  X(false, true, 2, 128, 1, false, false, 1)                                                         \
+  X(false, true, 2, 128, 2, false, false, 1)                                                         \
+  X(false, false, 4, 64, 1, false, false, 1)  /* bf16, κ·B_r in (256, 512]                        */ \
+  X(false, false, 4, 64, 2, false, false, 1)                                                         \
+  X(false, true, 4, 64, 1, false, false, 1)                                                          \
+  X(false, true, 4, 64, 2, false, false, 1) \
+  X(false, false, 1, 256, 1, false, false, 2) /* slot split: κ·B_r in (128, 512], row-major     */ \
+  X(false, false, 1, 256, 1, false, false, 4)                                                     \
+  X(false, false, 1, 128, 1, false, false, 2)                                                     \
+  X(false, false, 1, 128, 1, false, false, 4)                                                     \
+  X(true, false, 1, 128, 1, false, false, 2)                                                      \
+  X(true, false, 1, 128, 1, false, false, 4)
 
-template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL>
+template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL, int SS>
 int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, float* Y, int64_t ldy,
                 const Placement& pl, const HostPlan& hp, cudaStream_t st);
 
-#define BPS_TC_DECLARE(F, T, NM, B, C, TF_, RL_)                                                         \
-  extern template int launch_impl<F, T, NM, B, C, TF_, RL_>(const SketchParams&, const void*, int64_t, int64_t, \
+#define BPS_TC_DECLARE(F, T, NM, B, C, TF_, RL_, SS_)                                                    \
+  extern template int launch_impl<F, T, NM, B, C, TF_, RL_, SS_>(const SketchParams&, const void*, int64_t, int64_t, \
                                                             float*, int64_t, const Placement&, const HostPlan&, \
                                                             cudaStream_t);
 BPS_TC_INSTANTIATIONS(BPS_TC_DECLARE)

@@ -2,7 +2,8 @@
 // split across units so that nvcc compiles them in parallel.
 #include "bps_tc_kernel.cuh"
 
-BPS_TC_DEFINE(true, false, 1, 128, 1, true, false)
-BPS_TC_DEFINE(false, false, 1, 256, 1, false, false)
-BPS_TC_DEFINE(false, true, 1, 128, 1, false, true)
-BPS_TC_DEFINE(false, true, 2, 128, 1, false, false)
+BPS_TC_DEFINE(true, false, 1, 128, 1, true, false, 1)
+BPS_TC_DEFINE(false, false, 1, 256, 1, false, false, 1)
+BPS_TC_DEFINE(false, true, 1, 128, 1, false, true, 1)
+BPS_TC_DEFINE(false, true, 2, 128, 1, false, false, 1)
+BPS_TC_DEFINE(false, false, 1, 128, 1, false, false, 2)

@@ -2,7 +2,7 @@
 // split across units so that nvcc compiles them in parallel.
 #include "bps_tc_kernel.cuh"
 
-BPS_TC_DEFINE(true, false, 2, 64, 2, false, false)
-BPS_TC_DEFINE(false, false, 1, 64, 2, false, false)
-BPS_TC_DEFINE(false, true, 1, 128, 2, false, false)
-BPS_TC_DEFINE(false, true, 4, 64, 2, false, false)
+BPS_TC_DEFINE(true, false, 2, 64, 2, false, false, 1)
+BPS_TC_DEFINE(false, false, 1, 64, 2, false, false, 1)
+BPS_TC_DEFINE(false, true, 1, 128, 2, false, false, 1)
+BPS_TC_DEFINE(false, true, 4, 64, 2, false, false, 1)

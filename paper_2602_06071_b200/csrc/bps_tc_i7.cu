@@ -2,6 +2,7 @@
 // split across units so that nvcc compiles them in parallel.
 #include "bps_tc_kernel.cuh"
 
-BPS_TC_DEFINE(true, true, 2, 64, 2, false, false)
-BPS_TC_DEFINE(false, true, 1, 256, 2, false, true)
-BPS_TC_DEFINE(false, false, 2, 128, 2, false, false)
+BPS_TC_DEFINE(true, true, 2, 64, 2, false, false, 1)
+BPS_TC_DEFINE(false, true, 1, 256, 2, false, true, 1)
+BPS_TC_DEFINE(false, false, 2, 128, 2, false, false, 1)
+BPS_TC_DEFINE(false, false, 1, 256, 1, false, false, 4)

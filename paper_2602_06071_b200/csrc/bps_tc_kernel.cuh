@@ -58,8 +58,14 @@ constexpr int kMaxRanges = 511;           // canon: stream ranges per column til
 // roles take the last two warps): 0-3 epilogue (TMEM lane quarters 0-3) | 4-11 band
 // generator | 12-19 fp32 hi/lo converter (fp32 only) | NWARPS-2 TMA producer |
 // NWARPS-1 MMA issuer (+TMEM alloc).
-template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL = false>
+template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL = false, int SS = 1>
 struct Cfg {
+  // SS ("slot split", bf16/fp32 row-major NT form, κ·B_r in (128, 512]): the SS CTAs of a cluster
+  // take the same range and column tile and split the κ band slots — κ/SS slots (≤ 128 band rows,
+  // one M-tile) each; the data stage is loaded once from HBM and multicast to all of them (each
+  // CTA issues 1/SS of the rows).  Band sharing across column tiles (CS) is off then.
+  static_assert(SS == 1 || (CS == 1 && NMT == 1 && !TRANS && !TF && !RL), "SS: row-major NT form, one band tile");
+  static constexpr int CL = CS * SS;  // cluster size
   // RL ("re-layout", bf16 transposed layout only): TMA loads TWO K-chunks per box without
   // swizzle (256-byte runs per vector: with vectors megabytes apart, 128-byte runs stream at
   // ~4.6 TB/s and 256-byte runs at ~7.2 TB/s, scripts/tma_probe.cu), into two consecutive ring
@@ -335,10 +341,10 @@ __device__ float exact_elem(const TcArgs& a, int64_t i, uint32_t r, int64_t t, i
   return (float)(tot * (double)p.scale);
 }
 
-template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL>
-__global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREADS, 1)
+template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL, int SS>
+__global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTHREADS, 1)
     bps_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TcArgs args) {
-  using K = Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>;
+  using K = Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>;
   constexpr int BN = K::BN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -367,7 +373,11 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
   // ---- this CTA's column tile and input-stream range
   // canon: ranges partition the stream stages [0, stream_len·nk) at group granularity;
   // halo:  CTA rr owns outputs i ∈ [ilo, ihi) and streams positions ilo+1 .. ihi+κ-1 itself.
-  const int ct = blockIdx.x % args.nct, rr = blockIdx.x / args.nct;  // a cluster = CS consecutive tiles
+  // a cluster = CS consecutive column tiles (band sharing) or SS slot subsets of one tile (SS > 1)
+  const int css = SS > 1 ? (int)(blockIdx.x % SS) : 0;  // slot subset of this CTA
+  const int cid = SS > 1 ? (int)(blockIdx.x / SS) : (int)blockIdx.x;
+  const int ct = cid % args.nct, rr = cid / args.nct;
+  const uint32_t kap_l = kappa / SS, sig0 = (uint32_t)css * kap_l;  // this CTA's band slots [sig0, sig0 + kap_l)
   const int64_t col0 = (int64_t)ct * BN;
   // stage s ∈ [S0, S1) of the window = K-chunk s % nk of input position sb + s / nk
   int64_t sb, S0, S1, ilo = 0, ihi = 0;
@@ -390,7 +400,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
   if (threadIdx.x == 0) {
     for (int i = 0; i < K::NRAW; ++i) {
       ptx::mbar_init(&raw_full[i], 1);
-      ptx::mbar_init(&raw_empty[i], TF ? K::NCONVT : 1);  // TF: converters release raw stages
+      ptx::mbar_init(&raw_empty[i], TF ? K::NCONVT : SS);  // TF: converters; SS: every CTA's MMA (multicast data)
       ptx::mbar_init(&conv_full[i], K::NCONVT);
     }
     for (int i = 0; i < K::NBAND; ++i) {
@@ -412,7 +422,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
   if (threadIdx.x < 40) reinterpret_cast<uint32_t*>(smem + K::OFF_FIX)[threadIdx.x] = 0u;
   if (warp == K::W_MMA) ptx::tmem_alloc(tmem_ptr, K::TMEM_COLS);
   ptx::tc_fence_before();
-  if (CS > 1)
+  if (K::CL > 1)
     ptx::cluster_sync();  // peers' barriers are initialised before any remote copy/arrive
   else
     __syncthreads();
@@ -502,7 +512,21 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
               ptx::mbar_arrive_expect_tx(&raw_full[s], K::RAW_STAGE);
               uint8_t* dst = smem + K::OFF_RAW + s * K::RAW_STAGE;
               const int32_t r = (int32_t)(row0 + kc * kBK);
-              if (!TRANS) {
+              if (SS > 1) {
+                // slot split: this CTA loads rows [css·PR, (css+1)·PR) of the stage and multicasts them
+                // to the SS CTAs of the cluster (same smem offset, completing tx on each one's raw_full)
+                constexpr int PR = kBK / SS;
+                const uint16_t mask = (uint16_t)((1u << SS) - 1u);
+                const int32_t rp = r + css * PR;
+                if (F32) {
+                  ptx::tma_load_2d_mc(dst + css * PR * BN * 4, &tmap, &raw_full[s], (int32_t)col0, rp, mask, pol);
+                } else {
+#pragma unroll
+                  for (int b = 0; b < BN / 64; ++b)
+                    ptx::tma_load_2d_mc(dst + b * (kBK * 128) + css * PR * 128, &tmap, &raw_full[s], (int32_t)(col0 + 64 * b), rp,
+                                        mask, pol);
+                }
+              } else if (!TRANS) {
                 if (F32) {
                   ptx::tma_load_2d(dst, &tmap, &raw_full[s], (int32_t)col0, r, pol);
                 } else {
@@ -589,6 +613,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
             }
             if (TF)
               ptx::mma_commit(&ta_empty[(st - S0i) & 1]);
+            else if (SS > 1)
+              ptx::mma_commit_multicast(&dempty[ds], (uint16_t)((1u << SS) - 1u));  // every CTA's copy was filled
             else
               ptx::mma_commit(&dempty[ds]);
             if (CS > 1)
@@ -615,7 +641,10 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
       const int et = threadIdx.x;  // epilogue threads are 0..127
       uint32_t* fixmap = reinterpret_cast<uint32_t*>(smem + K::OFF_FIX);  // columns to recompute (BN bits)
       double* fixred = reinterpret_cast<double*>(smem + K::OFF_FIX + 64);
-      const int Br = (int)p.B_r, krows = (int)(kappa * p.B_r), kap = (int)kappa;
+      const int Br = (int)p.B_r, krows = (int)(kap_l * p.B_r), kap = (int)kappa, s0 = (int)sig0, kapl = (int)kap_l;
+      // slot of output i and whether this CTA holds it (always, unless slot split)
+      auto slot_of = [&](int i) { return (int)((uint32_t)(i + kap * 0x10000) % (uint32_t)kap); };
+      auto mine = [&](int i) { return SS == 1 || (slot_of(i) >= s0 && slot_of(i) < s0 + kapl); };
       const int sb_ = (int)sb, S0_ = (int)S0, S1_ = (int)S1, ilo_ = (int)ilo, ihi_ = (int)ihi;
       const int pb_ = (int)args.pos_begin, pe_ = (int)args.pos_end;
       auto first_stage = [&](int i) { return (i + 1 - sb_) * nk; };
@@ -753,7 +782,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
             while (t0 < 16 && c0 + t0 < krows) {
               const int sig = (c0 + t0) / Br, r0 = c0 + t0 - sig * Br;
               const int t1 = min(16, min(t0 + Br - r0, krows - c0));
-              const int i = slot_out(sig);
+              const int i = slot_out(s0 + sig);
               const int rl = role(i);
               if (rl == 1) {
                 const bool fin = blk_end && i == q - kap;
@@ -785,8 +814,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
           for (int m = 0; m < NMT; ++m) {
             const int rho = m * 128 + qtr * 32 + lane;
             const bool valid = rho < krows;
-            const int sig = valid ? rho / Br : 0, r = rho - sig * Br;
-            const int i = slot_out(sig);
+            const int sig = valid ? rho / Br : 0, r = rho - sig * Br;  // local slot
+            const int i = slot_out(s0 + sig);
             const int rl = valid ? role(i) : 0;
             const bool fin = rl == 1 && blk_end && i == q - kap;
             float* wcol = rl == 2 ? tile_ptr(rr, i - (q0c - kap), lg) + r : nullptr;  // column-major tile
@@ -833,7 +862,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
         ptx::tc_fence_before();
         ptx::mbar_arrive(&acc_free[db]);
         // ---- group-end bookkeeping (uniform over the 128 epilogue threads)
-        if (blk_end && role(q - kap) == 1 && bar_red_or(kEpiBar, 128, mybad)) fix_output(q - kap);
+        if (blk_end && mine(q - kap) && role(q - kap) == 1 && bar_red_or(kEpiBar, 128, mybad)) fix_output(q - kap);
       }
       tr.add(10, tstart);
       // canon, range end: every owned output still open parks its prefix (unscaled running sum) in
@@ -842,8 +871,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
         const int q_last = sb_ + (S1_ - 1) / nk;
         const bool full_end = (S1_ - 1) % nk == nk - 1;
         for (int i = q_last - kap + (full_end ? 1 : 0); i <= q_last - 1; ++i) {
-          if (role(i) != 1) continue;  // uniform
-          const int lo = (int)((uint32_t)i % (uint32_t)kap) * Br;
+          if (role(i) != 1 || !mine(i)) continue;  // uniform
+          const int lo = (slot_of(i) - s0) * Br;  // local band rows of its slot
           const int64_t yr0 = row0_of(i);
           if (TF) {
             const int64_t col = col0 + qtr * 32 + lane;
@@ -919,7 +948,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
         const int bt = threadIdx.x - 128;
         const uint32_t u = (uint32_t)bt & (kBK - 1);
         const uint32_t cg = (uint32_t)bt >> 6;  // 0..NCG-1
-        const uint32_t ncombo = kappa * p.s;
+        const uint32_t ncombo = kap_l * p.s;  // this CTA's (slot, chunk) combos
         const uint32_t T = ncombo > cg ? (ncombo - cg + K::NCG - 1) / K::NCG : 0;  // chunks of this thread (≤ 32)
         const bool zf = ncombo > 16u * K::NCG;  // stale rows no longer fit the prev registers (4 words)
         const uint32_t band_u32 = ptx::smem_u32(smem + K::OFF_BAND);
@@ -981,7 +1010,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
               // per input block q: hash key of chunk (σ, j): the output i ≡ σ (mod κ) fed by q is
               // i = q - ℓ with ℓ = ((q - σ - 1) mod κ) + 1
               for (uint32_t c = bt; c < ncombo; c += K::NBANDT) {
-                const uint32_t sig = c / p.s, j = c % p.s;
+                const uint32_t sig = sig0 + c / p.s, j = c % p.s;  // global slot
                 const uint32_t ell = mod_pos(q - (int64_t)sig - 1, kappa) + 1;
                 const uint32_t g = affine_pow(p, (uint64_t)mod_pos(q - (int64_t)ell, p.M), 0u);
                 const uint64_t key = (((uint64_t)g << 40) | ((uint64_t)(ell - 1) << 32) | (uint64_t)band_jfield(p, j)) ^ p.K;
@@ -1009,7 +1038,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
             }
             bool clear = local_no >= K::LOCALB;
             ++local_no;
-            const bool zero_fill = AFF ? kappa > 4u * K::NCG : (DENSE ? false : (zf && p.C > 1u));
+            const bool zero_fill = AFF ? kap_l > 4u * K::NCG : (DENSE ? false : (zf && p.C > 1u));
             if (zero_fill && clear) {
               // more stale entries per thread than the 4 prev words hold: zero-fill the stage
               // cooperatively, then write (one barrier per stage)
@@ -1091,7 +1120,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
   #pragma unroll
               for (int t = 0; t < 16; ++t) {
                 const uint32_t sig = cg + K::NCG * t;
-                if (sig >= kappa) break;
+                if (sig >= kap_l) break;
                 const uint32_t base = sig * p.B_r;
                 if (t < 4 && clear) {
                   const uint32_t w = prev[0][t & 3], a0 = w & 0xFFFFu;
@@ -1166,7 +1195,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
         }
         tr.add(8, tstart);
       };
-      const uint32_t ncomb = kappa * p.s;
+      const uint32_t ncomb = kap_l * p.s;
       if (p.mode)
         band_gen(std::true_type{}, std::integral_constant<int, 0>{});
       else if (p.C == 1u)
@@ -1321,7 +1350,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>::NTHREAD
   }
   const unsigned long long t_end0 = tr_cta.now();
   ptx::tc_fence_before();
-  if (CS > 1)
+  if (K::CL > 1)
     ptx::cluster_sync();  // no CTA leaves while peers may still copy into it or arrive on its barriers
   else
     __syncthreads();
@@ -1448,10 +1477,10 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 void* encode_tiled_entry();  // bps_tc.cu (thread-safe lazy driver entry point)
 
-template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL>
+template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL, int SS>
 int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, float* Y, int64_t ldy,
                 const Placement& pl, const HostPlan& hp, cudaStream_t st) {
-  using K = Cfg<F32, TRANS, NMT, BN_, CS, TF, RL>;
+  using K = Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>;
   constexpr int BN = K::BN;
   EncodeTiledFn enc = reinterpret_cast<EncodeTiledFn>(encode_tiled_entry());
   if (!enc) return fail(BPS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
@@ -1507,32 +1536,33 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
   int dev = 0;
   cudaGetDevice(&dev);
   int slots = hp.sms;
-  auto kern = bps_tc_kernel<F32, TRANS, NMT, BN_, CS, TF, RL>;
+  auto kern = bps_tc_kernel<F32, TRANS, NMT, BN_, CS, TF, RL, SS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
   if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-  if (CS > 1) {  // clusters must fit inside a GPC: not every SM can host one
+  if (K::CL > 1) {  // clusters must fit inside a GPC: not every SM can host one
     static std::atomic<int> cached_slots[64];
     int s = cached_slots[dev & 63].load(std::memory_order_relaxed);
     if (!s) {
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(CS * 64);
+      cfg.gridDim = dim3(K::CL * 64);
       cfg.blockDim = dim3(K::NTHREADS);
       cfg.dynamicSmemBytes = K::SMEM;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = CS;
+      at[0].val.clusterDim.x = K::CL;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
       int clusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) clusters = hp.sms / CS;
-      s = clusters * CS;
+      if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) clusters = hp.sms / K::CL;
+      s = clusters * K::CL;
       cached_slots[dev & 63].store(s, std::memory_order_relaxed);
     }
     slots = s;
   }
   a.canon = hp.canon;
+  slots /= SS;  // an SS cluster works on one (range, column tile)
   int64_t R = n_ct >= slots ? 1 : slots / n_ct;
   if (a.canon) {
     const int64_t NGt = a.stream_len * nk / hp.G;
@@ -1556,12 +1586,12 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     const int64_t NGt = a.stream_len * nk / hp.G;
     for (int64_t r = 0; r <= R; ++r) a.rb[r] = (int)(hp.G * (NGt * r / R));
   }
-  const int64_t grid = n_ct * R;
+  const int64_t grid = n_ct * R * SS;
   if (grid > 0x7FFFFFFF) return fail(BPS_ERR_UNSUPPORTED, "grid too large");
 
   if (a.canon) {
     a.tpc = tiles_per_cta(p, hp.G);
-    const size_t need = (size_t)grid * a.tpc * p.B_r * BN * 4;
+    const size_t need = (size_t)(grid / SS) * a.tpc * p.B_r * BN * 4;  // tiles indexed by (range, column tile)
     if (!hp.ws || hp.ws_bytes < need) return fail(BPS_ERR_INVALID_ARG, "workspace too small for the tc plan");
     a.W = reinterpret_cast<float*>(hp.ws);
   }
@@ -1577,7 +1607,7 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     dims[0] = (cuuint64_t)n;
     dims[1] = (cuuint64_t)in_rows;
     box[0] = F32 ? BN : 64;
-    box[1] = kBK * a.kgroup;
+    box[1] = SS > 1 ? kBK / SS : kBK * a.kgroup;  // SS: each CTA of the cluster loads 1/SS of the rows
   } else {
     dims[0] = (cuuint64_t)in_rows;  // coordinates (d)
     dims[1] = (cuuint64_t)n;        // vectors
@@ -1597,7 +1627,7 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     cudaLaunchAttribute at[1];
     int na = 0;
     at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = CS;
+    at[na].val.clusterDim.x = K::CL;
     at[na].val.clusterDim.y = 1;
     at[na].val.clusterDim.z = 1;
     ++na;
@@ -1668,7 +1698,7 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
 }  // namespace tcx
 }  // namespace bps
 
-#define BPS_TC_DEFINE(F, T, NM, B, C, TF_, RL_)                                                          \
-  template int bps::tcx::launch_impl<F, T, NM, B, C, TF_, RL_>(                                          \
+#define BPS_TC_DEFINE(F, T, NM, B, C, TF_, RL_, SS_)                                                     \
+  template int bps::tcx::launch_impl<F, T, NM, B, C, TF_, RL_, SS_>(                                     \
       const bps::SketchParams&, const void*, int64_t, int64_t, float*, int64_t, const bps::Placement&,   \
       const bps::tcx::HostPlan&, cudaStream_t);

@@ -152,14 +152,16 @@ def test_bf16_narrow(n):
                                     (64, 24, 1024, 16, 8)])
 @pytest.mark.parametrize("transposed", [False, True])
 def test_wide_band_bf16(layout, transposed):
-    """κ·B_r in (256, 512]: four band M-tiles (bf16 only, 64-column tiles). Selector columns must
-    reproduce S bit-exactly; Gaussian data meets the fp32 criterion against the bf16-rounded input."""
+    """κ·B_r in (256, 512]: row-major runs the slot-split form (4-CTA clusters, κ/4 slots each,
+    multicast data), transposed the four-band-tile form (bf16 only, 64-column tiles). Selector
+    columns must reproduce S bit-exactly; Gaussian data meets the fp32 criterion against the
+    bf16-rounded input."""
     M, Br, Bc, kappa, s = layout
     sk, osk = _pair(*layout, seed=21)
-    if (Br // s) & (Br // s - 1):  # C not a power of two: rejected by the tc variant
+    if ((Br // s) & (Br // s - 1)) and transposed:  # C not a power of two: the 4-tile form rejects it
         with pytest.raises(BpsError):
-            sk.apply(torch.zeros((sk.d, 8), device="cuda", dtype=torch.bfloat16), variant="tc")
-        return
+            sk.apply_t(torch.zeros((8, sk.d), device="cuda", dtype=torch.bfloat16), variant="tc")
+        return  # (row-major: the slot-split form covers it, checked below)
     rng = np.random.default_rng(1)
     J = rng.choice(sk.d, 40, replace=False)
     E = np.zeros((sk.d, len(J)), dtype=np.float32)
@@ -175,6 +177,25 @@ def test_wide_band_bf16(layout, transposed):
     Y = _run(sk, A.T if transposed else A, "tc", dtype=torch.bfloat16, transposed=transposed)
     Y = Y.T if transposed else Y
     assert_f32(Y, oracle.apply(osk, Ab), np.linalg.norm(Ab.astype(np.float64), axis=0), f"wide {layout} T={transposed}")
+
+
+@pytest.mark.parametrize("layout", [(32, 32, 2048, 16, 1), (32, 32, 2048, 16, 8), (64, 16, 1024, 16, 2),
+                                    (32, 32, 2048, 8, 4), (64, 24, 1024, 16, 8), (32, 48, 1024, 6, 3)])
+def test_slot_split_fp32(layout):
+    """fp32 row-major with κ·B_r in (128, 512]: the slot-split form (2- or 4-CTA clusters, κ/SS band
+    slots per CTA, TMA-multicast data) — bit-exact selector columns and the fp32 criterion."""
+    M, Br, Bc, kappa, s = layout
+    sk, osk = _pair(*layout, seed=22)
+    rng = np.random.default_rng(3)
+    J = rng.choice(sk.d, 40, replace=False)
+    E = np.zeros((sk.d, len(J)), dtype=np.float32)
+    E[J, np.arange(len(J))] = 1.0
+    Y = _run(sk, E, "tc")
+    Sref = oracle.apply(osk, E)
+    np.testing.assert_array_equal(np.sign(Y), np.sign(Sref))
+    assert np.all(np.abs(Y[Sref != 0]) == np.float32(1.0 / np.sqrt(kappa * s)))
+    A = synth.host_matrix("gaussian", sk.d, 200, seed=4)
+    assert_f32(_run(sk, A, "tc"), oracle.apply(osk, A), np.linalg.norm(A.astype(np.float64), axis=0), f"ss {layout}")
 
 
 def test_zero_n_and_zero_input():
