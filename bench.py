@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--ref-cols", type=int, default=64, help="reference arm: columns of the oracle sample per step")
     ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)  # launcher test without a GPU
     ap.add_argument("--no-strong", action="store_true", help="N>1 column mode: skip the strong-scaling measurement")
+    ap.add_argument("--n", type=int, default=0, help="override the config's column count (experiments)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -271,6 +272,8 @@ def main():
     from paper_2602_06071_b200 import configs as C
 
     cfg = C.CONFIGS[args.config]
+    if args.n:  # experiment: the config's sketch and d with another column count
+        cfg = cfg.with_(n=args.n, name=f"{cfg.name}_n{args.n}")
     if args.impl == "reference":
         reference_arm(args, cfg, rank)
         return

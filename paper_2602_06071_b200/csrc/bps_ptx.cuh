@@ -56,6 +56,25 @@ __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, u
   while (!mbar_try_wait_hint(bar, parity, ns)) {
   }
 }
+// two barriers checked by back-to-back try_waits (their latencies overlap): the MMA issuer needs
+// the data and the band stage of the same step
+__device__ __forceinline__ bool mbar_try_wait2(uint64_t* b1, uint32_t p1, uint64_t* b2, uint32_t p2) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 q, [%3], %4;\n\t"
+      "and.pred p, p, q;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(b1)), "r"(p1), "r"(smem_u32(b2)), "r"(p2)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait2(uint64_t* b1, uint32_t p1, uint64_t* b2, uint32_t p2) {
+  while (!mbar_try_wait2(b1, p1, b2, p2)) {
+  }
+}
 // waiting roles that are off the critical path back off so they do not steal issue slots
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
   while (!mbar_try_wait(bar, parity)) __nanosleep(ns);

@@ -88,7 +88,11 @@ struct Cfg {
 #define BPS_NBAND_CLUSTER 4
 #endif
   static constexpr int NBAND_CL = NMT == 1 ? BPS_NBAND_CLUSTER : (NMT == 2 ? 4 : 2);  // NMT = 4: 64 KB stages
-  static constexpr int NBAND = CS > 1 ? (NBAND_CL < CS ? CS : NBAND_CL) : ((NMT == 1 && !F32) ? 3 : 2);
+#ifndef BPS_NBAND_NARROW
+#define BPS_NBAND_NARROW 3
+#endif
+  static constexpr int NBAND = CS > 1 ? (NBAND_CL < CS ? CS : NBAND_CL)
+                                      : ((NMT == 1 && !F32) ? (BN_ <= 64 ? BPS_NBAND_NARROW : 3) : 2);
   static constexpr int LOCALB = NBAND / CS;  // band buffers this CTA generates into
   static constexpr int BUDGET = 210 * 1024;
   static constexpr int NRAW_FIT = (BUDGET - NBAND * BAND_STAGE) / RAW_STAGE;
@@ -169,11 +173,15 @@ struct TcArgs {
   int tbox;                    // transposed layout, kgroup > 1: vectors per TMA box (divides BN)
   int nohoist;                 // A/B knob: 1 disables the band generator's register-resident keys
   uint32_t mma_hint;           // MMA issuer's mbarrier suspend-time hint (ns)
+  uint32_t sleep_ns;           // TMA producer / band warps: back-off between polls of a not-yet-free
+                               // ring slot (0: poll with try_wait only)
   int ab;                      // A/B knob (env BPS_TC_AB): 2 skip contributor tile writes (results
                                // wrong), 4 evict_normal for partials, 8 combine with 128 threads,
-                               // 16 combine without programmatic dependent launch, 32 skip the main kernel
+                               // 16 combine without programmatic dependent launch, 32 skip the main kernel,
+                               // 64 combine element parts not capped at one wave
   int dbg;  // experiment switches (env BPS_TC_DEBUG; 0 in production): 1 no band, 2 no convert, 4 no MMA,
-            // 8 cycle trace, 16 no band proxy fence, 32 band without hashing
+            // 8 cycle trace, 16 no band proxy fence, 32 band without hashing,
+            // 64 (with 4) ring slots released by thread arrives instead of tcgen05.commit
   unsigned long long* trace;   // dbg & 8: per-CTA cycle counters (16 per CTA), else nullptr
 };
 
@@ -283,6 +291,30 @@ __device__ __forceinline__ float ld_cg_f(const float* p) {
   return v;
 }
 // named-barrier OR reduction over `n` threads (bar.red.or)
+// Arrival of a whole warp on an mbarrier counted in warps (BPS_WARP_ARRIVE): the lanes' prior
+// shared-memory / TMEM accesses are ordered before lane 0's release-arrive by __syncwarp, so the
+// barrier sees one arrival per warp instead of 32 (per-thread arrivals on one barrier serialise
+// in the barrier unit; 256 of them per stage bounded the narrow-tile pipeline).
+#ifndef BPS_WARP_ARRIVE
+#define BPS_WARP_ARRIVE 1
+#endif
+constexpr int kArrivePerWarp = BPS_WARP_ARRIVE ? 1 : 32;
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
+#if BPS_WARP_ARRIVE
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(bar);
+#else
+  ptx::mbar_arrive(bar);
+#endif
+}
+
+__device__ __forceinline__ void wait_slot(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  if (ns)
+    ptx::mbar_wait_sleep(bar, parity, ns);
+  else
+    ptx::mbar_wait(bar, parity);
+}
+
 __device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t n, bool v) {
   uint32_t r;
   asm volatile(
@@ -400,11 +432,11 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
   if (threadIdx.x == 0) {
     for (int i = 0; i < K::NRAW; ++i) {
       ptx::mbar_init(&raw_full[i], 1);
-      ptx::mbar_init(&raw_empty[i], TF ? K::NCONVT : SS);  // TF: converters; SS: every CTA's MMA (multicast data)
-      ptx::mbar_init(&conv_full[i], K::NCONVT);
+      ptx::mbar_init(&raw_empty[i], TF ? K::NCONVW * kArrivePerWarp : SS);  // TF: converter warps; SS: every CTA's MMA
+      ptx::mbar_init(&conv_full[i], K::NCONVW > 0 ? K::NCONVW * kArrivePerWarp : 1);
     }
     for (int i = 0; i < K::NBAND; ++i) {
-      ptx::mbar_init(&band_full[i], CS > 1 ? 1 : K::NBANDT);
+      ptx::mbar_init(&band_full[i], CS > 1 ? 1 : K::NBW * kArrivePerWarp);
       ptx::mbar_init(&band_empty[i], CS);
     }
     for (int i = 0; i < K::NACC; ++i) {
@@ -412,7 +444,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
       ptx::mbar_init(&acc_free[i], 128);
     }
     for (int i = 0; i < K::NCONVA; ++i) {
-      ptx::mbar_init(&ta_full[i], K::NCONVT);
+      ptx::mbar_init(&ta_full[i], K::NCONVW > 0 ? K::NCONVW * kArrivePerWarp : 1);
       ptx::mbar_init(&ta_empty[i], 1);
     }
     ptx::mbar_init(ta_empty + K::NCONVA, 1);  // epilogue tail
@@ -452,8 +484,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               // one unswizzled box = K-chunks kc, kc+1 of BN vectors (256 B per vector) into ring
               // slots s, s+1 (contiguous: NRAW is even and pairs start at even slots)
               if ((kc & 1) == 0) {
-                ptx::mbar_wait_sleep(&raw_empty[s], ph ^ 1, 20);
-                ptx::mbar_wait_sleep(&raw_empty[s + 1], ph ^ 1, 20);
+                wait_slot(&raw_empty[s], ph ^ 1, args.sleep_ns);
+                wait_slot(&raw_empty[s + 1], ph ^ 1, args.sleep_ns);
                 tr.add(0, t0);
                 ptx::mbar_arrive_expect_tx(&raw_full[s], 2 * K::RAW_STAGE);
                 ptx::tma_load_2d(smem + K::OFF_RAW + s * K::RAW_STAGE, &tmap, &raw_full[s], (int32_t)(row0 + kc * kBK),
@@ -468,7 +500,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
                 int s2 = s;
                 uint32_t ph2 = ph;
                 for (int i = 0; i < args.kgroup; ++i) {
-                  ptx::mbar_wait_sleep(&raw_empty[s2], ph2 ^ 1, 20);
+                  wait_slot(&raw_empty[s2], ph2 ^ 1, args.sleep_ns);
                   if (++s2 == K::NRAW) s2 = 0, ph2 ^= 1;
                 }
                 tr.add(0, t0);
@@ -489,7 +521,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
                 int s2 = s;
                 uint32_t ph2 = ph;
                 for (int i = 0; i < m; ++i) {
-                  ptx::mbar_wait_sleep(&raw_empty[s2], ph2 ^ 1, 20);
+                  wait_slot(&raw_empty[s2], ph2 ^ 1, args.sleep_ns);
                   ptx::mbar_arrive_expect_tx(&raw_full[s2], K::RAW_STAGE);
                   if (++s2 == K::NRAW) s2 = 0, ph2 ^= 1;
                 }
@@ -507,7 +539,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               --grp;
               tr.add(0, t0);
             } else {
-              ptx::mbar_wait_sleep(&raw_empty[s], ph ^ 1, 20);
+              wait_slot(&raw_empty[s], ph ^ 1, args.sleep_ns);
               tr.add(0, t0);
               ptx::mbar_arrive_expect_tx(&raw_full[s], K::RAW_STAGE);
               uint8_t* dst = smem + K::OFF_RAW + s * K::RAW_STAGE;
@@ -559,6 +591,14 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         const uint32_t data_base = ptx::smem_u32(smem + K::OFF_RAW);
         constexpr int DSTAGE = K::RAW_STAGE;
         const uint32_t band_base = ptx::smem_u32(smem + K::OFF_BAND);
+        // Descriptors are built once: per stage only the low word (start address >> 4, 14 bits; smem
+        // addresses < 228 KB never carry out of it) moves by the ring slot and the K-step.  Rebuilding
+        // them per MMA was a ~45-instruction dependent uniform-datapath chain per stage that bounded
+        // the narrow-tile pipeline (~650 cycles of issue per 64-row stage, ncu source view).
+        const uint64_t a0 = ptx::smem_desc_sw128(band_base, 0, 1024);  // band, K-major
+        const uint64_t b0 = TRANS ? ptx::smem_desc_sw128(data_base, 0, 1024) : ptx::smem_desc_sw128(data_base, kBK * 128, 1024);
+        const uint32_t a0lo = (uint32_t)a0, b0lo = (uint32_t)b0;
+        const uint64_t a0hi = a0 & 0xFFFFFFFF00000000ull, b0hi = b0 & 0xFFFFFFFF00000000ull;
         int gcount = 0, dbuf = 0;  // groups started; D buffer of the current group
         int kc = S0i % nk;
         int gi = kc % G;  // position inside the accumulation group (groups restart at block starts)
@@ -576,23 +616,22 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               }
             }
             unsigned long long t0 = tr.now();
-            if (TF)
-              ptx::mbar_wait(&ta_full[(st - S0i) & 1], (uint32_t)((st - S0i) >> 1) & 1u);
-            else
-              ptx::mbar_wait_hint(&dfull[(!TRANS && args.kgroup > 1) ? (ds & ~(args.kgroup - 1)) : ds], dph, args.mma_hint);
+            {
+              // data stage and band stage of this step, polled together
+              uint64_t* db = TF ? &ta_full[(st - S0i) & 1] : &dfull[(!TRANS && args.kgroup > 1) ? (ds & ~(args.kgroup - 1)) : ds];
+              const uint32_t dp = TF ? ((uint32_t)((st - S0i) >> 1) & 1u) : dph;
+              ptx::mbar_wait2(db, dp, &band_full[bs], bph);
+            }
             tr.add(3, t0);
-            t0 = tr.now();
-            ptx::mbar_wait_hint(&band_full[bs], bph, args.mma_hint);
-            tr.add(4, t0);
             ptx::tc_fence_after();
-            const uint32_t dbase = data_base + ds * DSTAGE;
-            const uint32_t bbase = band_base + bs * K::BAND_STAGE;
+            const uint32_t alo = a0lo + (uint32_t)bs * (uint32_t)(K::BAND_STAGE >> 4);
+            const uint32_t blo = b0lo + (uint32_t)ds * (uint32_t)(DSTAGE >> 4);
             if (ptx::elect_one()) {
             if (TF) {
               const uint32_t ta = tmem_A + (uint32_t)((st - S0i) & 1) * 64;
 #pragma unroll
               for (int ks = 0; ks < kBK / 16; ++ks) {
-                const uint64_t bdesc = ptx::smem_desc_sw128(bbase + ks * 32, 0, 1024);  // band, K-major
+                const uint64_t bdesc = a0hi | (alo + ks * 2);  // band, K-major: +32 B per K-step
                 if (!BPS_DBG(4)) {
                   const uint32_t dt = tmem + (dbuf ? K::OFF_D1 : 0);
                   ptx::mma_bf16_ts(dt, ta + ks * 8, bdesc, K::IDESC, (gstart && ks == 0) ? 0u : 1u);  // hi
@@ -604,20 +643,25 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
             for (int ks = 0; ks < kBK / 16; ++ks) {
 #pragma unroll
               for (int m = 0; m < NMT; ++m) {
-                const uint64_t adesc = ptx::smem_desc_sw128(bbase + m * kBandTile + ks * 32, 0, 1024);
-                const uint64_t bdesc = TRANS ? ptx::smem_desc_sw128(dbase + ks * 32, 0, 1024)
-                                             : ptx::smem_desc_sw128(dbase + ks * 16 * 128, kBK * 128, 1024);
+                const uint64_t adesc = a0hi | (alo + (uint32_t)(m * (kBandTile >> 4) + ks * 2));
+                // data: K-major (+32 B per K-step) or MN-major (+16 rows of 128 B per K-step)
+                const uint64_t bdesc = b0hi | (blo + (uint32_t)(TRANS ? ks * 2 : ks * 128));
                 const uint32_t acc = (gstart && ks == 0) ? 0u : 1u;  // fresh per group
                 if (!BPS_DBG(4)) ptx::mma_bf16_ss(tmem + m * K::DN, adesc, bdesc, K::IDESC, acc);
               }
             }
-            if (TF)
+            if (BPS_DBG(64)) {  // experiment (with dbg 4, no MMA issued): release by a thread arrive
+              ptx::mbar_arrive(TF ? &ta_empty[(st - S0i) & 1] : &dempty[ds]);
+              ptx::mbar_arrive(&band_empty[bs]);
+            } else if (TF)
               ptx::mma_commit(&ta_empty[(st - S0i) & 1]);
             else if (SS > 1)
               ptx::mma_commit_multicast(&dempty[ds], (uint16_t)((1u << SS) - 1u));  // every CTA's copy was filled
             else
               ptx::mma_commit(&dempty[ds]);
-            if (CS > 1)
+            if (BPS_DBG(64))
+              ;
+            else if (CS > 1)
               ptx::mma_commit_multicast(&band_empty[bs], (uint16_t)((1u << CS) - 1));
             else
               ptx::mma_commit(&band_empty[bs]);
@@ -1003,7 +1047,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
           {
             const bool local = CS == 1 || (uint32_t)bs % CS == crank;
             unsigned long long t0 = tr.now();
-            if (local || bt == 0) ptx::mbar_wait_sleep(&band_empty[bs], bph ^ 1, 20);
+            if (local || bt == 0) wait_slot(&band_empty[bs], bph ^ 1, args.sleep_ns);
             tr.add(6, t0);
             t0 = tr.now();
             if (kc == 0 || st == S0i) {
@@ -1050,7 +1094,9 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
             uint32_t nw[NPW];
   #pragma unroll
             for (int w = 0; w < NPW; ++w) nw[w] = 0;
-            if constexpr (DENSE) {
+            if (BPS_DBG(1)) {
+              // experiment: no band generation (every generator variant)
+            } else if constexpr (DENSE) {
               // C = B_r/s ∈ {1, 2, 4}: chunk c owns the CP band rows crow[c] .. +CP-1 and has exactly
               // one ±1 per column among them, so every row of the chunk is rewritten each stage as
               // whole 16-byte SW128 pieces (8 columns): per item (chunk, 8-column group) 8
@@ -1188,7 +1234,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
                 ptx::mbar_arrive(&band_full[bs]);
               }
             } else {
-              ptx::mbar_arrive(&band_full[bs]);
+              warp_arrive(&band_full[bs]);
             }
             if (++bs == K::NBAND) bs = 0, bph ^= 1;
           }
@@ -1230,7 +1276,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         float a[32];
 #pragma unroll
         for (int r = 0; r < 32; ++r) a[r] = raw[r * BN];
-        ptx::mbar_arrive(&raw_empty[rs]);  // values are in registers
+        warp_arrive(&raw_empty[rs]);  // values are in registers
         if (++rs == K::NRAW) rs = 0, rph ^= 1;
         const uint32_t ab = (uint32_t)(it & 1);
         ptx::mbar_wait(&ta_empty[ab], (uint32_t)((it >> 1) & 1) ^ 1u);
@@ -1248,7 +1294,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         ptx::tmem_st16(ta + lane_off + 32, lo);
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&ta_full[ab]);
+        warp_arrive(&ta_full[ab]);
         (void)cv;
       }
     } else if (RL && warp >= K::W_CONV0 && warp < K::W_CONV0 + K::NCONVW) {
@@ -1277,8 +1323,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
           *reinterpret_cast<uint4*>(base + (c >> 3) * K::RAW_STAGE + v * 128u + (((c & 7u) ^ (v & 7u)) << 4)) = a[i];
         }
         ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&conv_full[rs]);
-        ptx::mbar_arrive(&conv_full[rs + 1]);
+        warp_arrive(&conv_full[rs]);
+        warp_arrive(&conv_full[rs + 1]);
         rs += 2;
         if (rs == K::NRAW) rs = 0, rph ^= 1;
       }
@@ -1342,7 +1388,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
           *reinterpret_cast<uint2*>(hbase + K::CONV_HALF + i * istep) = make_uint2(l01, l23);
         }
         ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&conv_full[rs]);
+        warp_arrive(&conv_full[rs]);
         if (++rs == K::NRAW) rs = 0, rph ^= 1;
       }
       tr.add(12, tstart);
@@ -1378,10 +1424,11 @@ __global__ void __launch_bounds__(256) bps_tc_combine(const __grid_constant__ Tc
   __shared__ uint32_t fixmap[8];
   __shared__ double red[4];
   __shared__ const float* tiles[kCombineMaxTiles];
+  __shared__ int srb[kMaxRanges + 1];
   __shared__ int ntiles;
   const SketchParams& p = args.p;
   const int nk = (int)(p.B_c / kBK);
-  const CanonGeom geo(args, nk, BN);
+  CanonGeom geo(args, nk, BN);
   // blockIdx.x = (output o, column tile ct, element part): each CTA takes 1/nsplit of the tile's
   // elements, at most EPT per thread, so that all of them are in flight in one pass
   const unsigned nsplit = gridDim.y;
@@ -1389,8 +1436,13 @@ __global__ void __launch_bounds__(256) bps_tc_combine(const __grid_constant__ Tc
   const int part = (int)blockIdx.y;
   const int i = (int)args.i_first + o;  // owner coordinates (first stage o·nk ≥ 0)
   const int F = geo.first_stage(i);
-  if (F + geo.KN <= geo.range_begin(geo.range_of(F) + 1)) return;  // finished by its owner
+  // the range starts, staged in shared memory: the walk's binary searches on the kernel parameter
+  // space (dynamically indexed constant loads, one dependent miss per step) serialised every CTA
+  for (int r = (int)threadIdx.x; r <= geo.R; r += (int)blockDim.x) srb[r] = args.rb[r];
   if (threadIdx.x < 8) fixmap[threadIdx.x] = 0u;
+  __syncthreads();
+  geo.rb = srb;
+  if (F + geo.KN <= geo.range_begin(geo.range_of(F) + 1)) return;  // finished by its owner
   if (threadIdx.x == 0) {
     int nt = 0;
     geo.walk(i, [&](int r_, int j, int ngr) {
@@ -1523,6 +1575,7 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
   a.nohoist = getenv("BPS_TC_NOHOIST") ? 1 : 0;
   a.ab = getenv("BPS_TC_AB") ? atoi(getenv("BPS_TC_AB")) : 0;
   a.mma_hint = getenv("BPS_TC_MMA_HINT") ? (uint32_t)atoi(getenv("BPS_TC_MMA_HINT")) : 0u;  // A/B knob
+  a.sleep_ns = getenv("BPS_TC_SLEEP") ? (uint32_t)atoi(getenv("BPS_TC_SLEEP")) : 20u;  // A/B knob
   a.tbox = BN;
   if (const char* e = getenv("BPS_TC_TBOX")) a.tbox = atoi(e);  // tuning knob (transposed layout)
   if (a.tbox < 8 || BN % a.tbox || a.tbox % 8 || a.kgroup == 1) a.tbox = BN;
@@ -1675,7 +1728,13 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     if (cgrid > 0x7FFFFFFF) return fail(BPS_ERR_UNSUPPORTED, "combine grid too large");
     cudaLaunchConfig_t cfg = {};
     const int cthreads = (a.ab & 8) ? 128 : 256;
-    const int nsplit = (int)std::max<int64_t>(1, ((int64_t)p.B_r * BN + cthreads * 4 - 1) / (cthreads * 4));
+    // element parts per (output, column tile): all of a tile's elements in flight at once, unless that
+    // takes more than one wave of co-resident CTAs (5 per SM at 48 registers): every CTA walks its
+    // output's segment list serially before loading, so extra waves cost a walk each (ncu: 2.8 waves
+    // at 4 parts on LS, a third of the samples waiting on that walk)
+    int nsplit = (int)std::max<int64_t>(1, ((int64_t)p.B_r * BN + cthreads * 4 - 1) / (cthreads * 4));
+    const int64_t resident = (int64_t)hp.sms * ((a.ab & 8) ? 10 : 5);
+    if (!(a.ab & 64)) nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit, resident / std::max<int64_t>(1, cgrid)));
     cfg.gridDim = dim3((unsigned)cgrid, (unsigned)std::min(nsplit, 65535));
     cfg.blockDim = dim3(cthreads);
     cfg.stream = st;

@@ -1,7 +1,7 @@
 #!/bin/bash
 # ncu launch list (kernel durations, cold cache, serialised) of a few bench steps
 O=gpurun_out; T=${TAG:-ll}; C=${CFG:-ls}
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none ${NCUX} -c ${NK:-40} --csv --log-file $O/${T}_launches_${C}.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none ${NCUX:--k regex:bps} -c ${NK:-40} --csv --log-file $O/${T}_launches_${C}.csv \
    env $LENV python bench.py --config $C --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks $BARGS > /dev/null 2>&1
 echo "ncu rc=$?"
 python - "$O/${T}_launches_${C}.csv" <<'PY'

@@ -33,7 +33,7 @@ python bench.py --impl reference > $O/${TAG}_bench_reference.json 2>&1
 fi
 if [ -n "$NCU" ]; then
   for c in ls grad smalln; do
-    timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 60 --csv \
+    timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:bps -c 20 --csv \
        --log-file $O/${TAG}_launches_${c}.csv python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-clocks > /dev/null 2>&1
     echo "ncu launches $c rc=$?"
   done

@@ -26,7 +26,10 @@ check((16, 32, 1024, 4, 4), 200, ws=False)          # halo ranges
 check((16, 32, 1024, 4, 4), 130, transposed=True)   # fp32 transposed NT
 check((64, 16, 512, 8, 2), 136, dt="bf16")          # bf16 NT
 check((64, 16, 512, 8, 2), 64, dt="bf16", transposed=True)  # bf16 transposed re-layout
-check((32, 32, 2048, 16, 4), 64, dt="bf16")         # four band tiles
+check((32, 32, 2048, 16, 4), 64, dt="bf16")         # kappa*B_r = 512 row-major: slot-split 4-CTA cluster
+check((32, 32, 2048, 16, 4), 128)                   # fp32 slot split
+check((32, 32, 2048, 8, 4), 128, dt="bf16")         # kappa*B_r = 256: slot-split pair
+check((32, 32, 2048, 16, 4), 64, dt="bf16", transposed=True)  # four band tiles (transposed)
 check((16, 32, 1024, 4, 8), 64, dt="bf16", mode="affine")
 check((8, 32, 128, 2, 2), 16, variant="sparse")
 check((8, 32, 128, 2, 2), 16, variant="sparse", transposed=True)

@@ -14,8 +14,8 @@ for name in sys.argv[1:] or ["ls", "grad"]:
     os.environ["BPS_TC_DEBUG"] = "0"
     for _ in range(3): sk.apply(A, out=Y)
     torch.cuda.synchronize()
-    os.environ["BPS_TC_DEBUG"] = "8"
-    print("====", name, flush=True)
+    os.environ["BPS_TC_DEBUG"] = os.environ.get("TRACE_DBG", "8")
+    print("====", name, "dbg", os.environ["BPS_TC_DEBUG"], flush=True)
     sk.apply(A, out=Y)
     torch.cuda.synchronize()
     sys.stderr.flush()

@@ -3,7 +3,7 @@
 // CTA (tile, range) streams boxes of BOXK elements × BOXR vectors along its d-range through a
 // 4-deep smem ring; a consumer thread releases each stage as soon as it lands.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tma_probe scripts/tma_probe.cu -lcuda
-//   ./tma_probe d n boxr boxk swizzle(0/1) [ctas]
+//   ./tma_probe d n boxr boxk swizzle(0/1) [ctas] [ring depth]
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -15,7 +15,7 @@
 
 using namespace bps;
 
-constexpr int NST = 4;
+constexpr int NSTMAX = 64;  // ring depth: argv[7] (default 4)
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, uint64_t* bar, int32_t c0, int32_t c1, int32_t c2,
                                             uint64_t pol) {
@@ -27,10 +27,10 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, uint64_
 }
 
 __global__ void __launch_bounds__(64, 1) probe(const __grid_constant__ CUtensorMap tm, int d, int n, int boxr, int boxk,
-                                               int ntiles, int R, int stage_bytes) {
+                                               int ntiles, int R, int stage_bytes, int NST) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full[NST], empty[NST];
+  __shared__ uint64_t full[NSTMAX], empty[NSTMAX];
   const bool rowmajor = ntiles == 0;  // rows of d elements (d ≤ boxk), CTAs stream row boxes
   const int tile = rowmajor ? 0 : blockIdx.x % ntiles, rr = rowmajor ? blockIdx.x : blockIdx.x / ntiles;
   const int64_t nk = rowmajor ? (int64_t)n / boxr : d / (boxk < 0 ? -boxk : boxk);
@@ -74,6 +74,7 @@ int main(int argc, char** argv) {
   const int64_t d = atoll(argv[1]), n = atoll(argv[2]);
   const int boxr = atoi(argv[3]), boxk = atoi(argv[4]), swz = atoi(argv[5]);
   int ctas = argc > 6 ? atoi(argv[6]) : 148;
+  const int NST = argc > 7 ? atoi(argv[7]) : 4;
   void* X;
   if (cudaMalloc(&X, d * n * 2) != cudaSuccess) return 1;
   cudaMemset(X, 0, d * n * 2);
@@ -108,17 +109,17 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int w = 0; w < 2; ++w) probe<<<grid, 64, smem>>>(tm, (int)d, (int)n, boxr, boxk, ntiles, R, sb);
+  for (int w = 0; w < 2; ++w) probe<<<grid, 64, smem>>>(tm, (int)d, (int)n, boxr, boxk, ntiles, R, sb, NST);
   cudaEventRecord(e0);
   const int it = 5;
-  for (int w = 0; w < it; ++w) probe<<<grid, 64, smem>>>(tm, (int)d, (int)n, boxr, boxk, ntiles, R, sb);
+  for (int w = 0; w < it; ++w) probe<<<grid, 64, smem>>>(tm, (int)d, (int)n, boxr, boxk, ntiles, R, sb, NST);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
   const double bytes = (double)d * n * 2;
-  printf("d=%lld n=%lld boxr=%d boxk=%d swz=%d grid=%d (tiles %d x ranges %d): %.3f ms  %.0f GB/s  err=%s\n",
-         (long long)d, (long long)n, boxr, boxk, swz, grid, ntiles, R, ms / it, bytes / (ms / it * 1e-3) / 1e9,
+  printf("nst=%d d=%lld n=%lld boxr=%d boxk=%d swz=%d grid=%d (tiles %d x ranges %d): %.3f ms  %.0f GB/s  err=%s\n",
+         NST, (long long)d, (long long)n, boxr, boxk, swz, grid, ntiles, R, ms / it, bytes / (ms / it * 1e-3) / 1e9,
          cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
