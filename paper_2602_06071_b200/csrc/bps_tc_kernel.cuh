@@ -170,6 +170,7 @@ struct TcArgs {
   int64_t tpc;                 // canon: tiles per CTA
   int G;                       // K-chunks per accumulation group (divides B_c/64; sketch-only)
   int kgroup;                  // transposed layout: K-chunks whose TMA loads are issued together (≤ NRAW)
+  int kstep;                   // stages per band/MMA handshake (1 or 2; 2: narrow bf16 tile, see bps_tc_kernel)
   int tbox;                    // transposed layout, kgroup > 1: vectors per TMA box (divides BN)
   int nohoist;                 // A/B knob: 1 disables the band generator's register-resident keys
   uint32_t mma_hint;           // MMA issuer's mbarrier suspend-time hint (ns)
@@ -600,6 +601,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         const uint32_t a0lo = (uint32_t)a0, b0lo = (uint32_t)b0;
         const uint64_t a0hi = a0 & 0xFFFFFFFF00000000ull, b0hi = b0 & 0xFFFFFFFF00000000ull;
         int gcount = 0, dbuf = 0;  // groups started; D buffer of the current group
+        const int ksm = args.kstep - 1;
         int kc = S0i % nk;
         int gi = kc % G;  // position inside the accumulation group (groups restart at block starts)
         for (int st = S0i; st < S1i; ++st) {
@@ -616,7 +618,10 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               }
             }
             unsigned long long t0 = tr.now();
-            {
+            // kstep = 2 (narrow tile): one handshake per pair of stages — the TMA box of the pair
+            // completes on its first slot and the band warps arrive once, on the pair's first buffer
+            const int sp = (st - S0i) & ksm;  // position of this stage in its step
+            if (sp == 0) {
               // data stage and band stage of this step, polled together
               uint64_t* db = TF ? &ta_full[(st - S0i) & 1] : &dfull[(!TRANS && args.kgroup > 1) ? (ds & ~(args.kgroup - 1)) : ds];
               const uint32_t dp = TF ? ((uint32_t)((st - S0i) >> 1) & 1u) : dph;
@@ -659,12 +664,12 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               ptx::mma_commit_multicast(&dempty[ds], (uint16_t)((1u << SS) - 1u));  // every CTA's copy was filled
             else
               ptx::mma_commit(&dempty[ds]);
-            if (BPS_DBG(64))
-              ;
+            if (BPS_DBG(64) || sp != ksm)
+              ;  // kstep = 2: the pair's buffers are released together, on its first buffer
             else if (CS > 1)
               ptx::mma_commit_multicast(&band_empty[bs], (uint16_t)((1u << CS) - 1));
             else
-              ptx::mma_commit(&band_empty[bs]);
+              ptx::mma_commit(&band_empty[bs - ksm]);
             if (gend) ptx::mma_commit(&acc_full[dbuf]);
             }  // elect_one
             __syncwarp();
@@ -1037,6 +1042,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         int bs = 0;
         uint32_t bph = 0;
         int stage_no = 0;
+        const int ksm = args.kstep - 1;
         const Tr tr((args.trace && bt == 0) ? args.trace + blockIdx.x * kTrSlots : nullptr);
         const unsigned long long tstart = tr.now();
         int kc = S0i % nk;
@@ -1046,8 +1052,9 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
           uint64_t* ck = ckey + par * 256;
           {
             const bool local = CS == 1 || (uint32_t)bs % CS == crank;
+            const int sp = stage_no & ksm;  // kstep = 2: wait at the first stage of a pair only
             unsigned long long t0 = tr.now();
-            if (local || bt == 0) wait_slot(&band_empty[bs], bph ^ 1, args.sleep_ns);
+            if ((local || bt == 0) && sp == 0) wait_slot(&band_empty[bs], bph ^ 1, args.sleep_ns);
             tr.add(6, t0);
             t0 = tr.now();
             if (kc == 0 || st == S0i) {
@@ -1221,6 +1228,10 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               for (int w = 0; w < NPW; ++w) prev[b][w] = prev[b + 1][w];
   #pragma unroll
             for (int w = 0; w < NPW; ++w) prev[K::LOCALB - 1][w] = nw[w];
+            if (sp != ksm) {  // kstep = 2: first stage of a pair — fence and arrive after the second
+              if (++bs == K::NBAND) bs = 0, bph ^= 1;
+              continue;
+            }
             if (!BPS_DBG(16)) ptx::fence_proxy_async_smem();
             if (CS > 1) {
               ptx::named_bar_sync(3, K::NBANDT);  // whole stage written (and fenced) by all band threads
@@ -1234,7 +1245,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
                 ptx::mbar_arrive(&band_full[bs]);
               }
             } else {
-              warp_arrive(&band_full[bs]);
+              warp_arrive(&band_full[bs - ksm]);
             }
             if (++bs == K::NBAND) bs = 0, bph ^= 1;
           }
@@ -1571,6 +1582,15 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     // measured no gain on smalln, off by default); a box group never straddles an accumulation group
     if (F32 || BN != 64 || hp.G % a.kgroup || K::NRAW % a.kgroup || a.kgroup > 4 || (a.kgroup & (a.kgroup - 1)))
       a.kgroup = 1;
+  }
+  // narrow bf16 tile: stage pairs share one data barrier (a 128-row TMA box) and one band
+  // handshake, halving the per-stage synchronisation that bounds it (profiles/r02_narrow_n.md);
+  // pairs never straddle an accumulation group, block or range (G, nk even; ranges start at groups)
+  a.kstep = 1;
+  if (!F32 && !TRANS && BN == 64 && CS == 1 && SS == 1 && NMT == 1 && K::NBAND % 2 == 0 && K::NRAW % 2 == 0 &&
+      hp.G % 2 == 0 && nk % 2 == 0 && !getenv("BPS_TC_KSTEP1")) {
+    a.kstep = 2;
+    a.kgroup = 2;
   }
   a.nohoist = getenv("BPS_TC_NOHOIST") ? 1 : 0;
   a.ab = getenv("BPS_TC_AB") ? atoi(getenv("BPS_TC_AB")) : 0;
