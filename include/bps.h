@@ -236,6 +236,34 @@ int bps_orbit_range_workspace_size(const bps_sketch* sk, int64_t pos_begin, int6
                                    bps_dtype dtype, size_t* bytes);
 
 /*
+ * bps_apply_orbit_range_bcast — bps_apply_orbit_range_ws whose output is ALSO written into other
+ *   buffers by the kernel epilogue itself: the all-gather step of orbit block sharding
+ *   (rank r's output rows must reach every rank) fused into the
+ *   store of each finished output tile, instead of a separate NCCL pass.
+ *   dst:      host array of ndst (0..8) device pointers, each the base of a row-major fp32
+ *             destination with leading dimension ld_dst (≥ n, 16-byte multiple) — typically the
+ *             peers' symmetric buffers (CUDA IPC / symmetric-memory mappings of other GPUs'
+ *             memory over NVLink), or local buffers.  Caller-owned; must be writable from the
+ *             current device and not overlap Y_local, A_local or the workspace.
+ *   mc_dst:   NULL, or an NVLS multicast address of such a buffer (one multimem.st reaches every
+ *             GPU bound to the multicast object).
+ *   dst_row0: row of the destinations receiving Y_local's row 0 (block sharding: the rank's first
+ *             orbit position × B_r in an orbit-ordered k × n buffer).
+ *   Y_local is written as in bps_apply_orbit_range_ws (it also holds the range's parked prefixes).
+ *   Every destination receives bitwise the values of Y_local.  The tcgen05 variant stores to the
+ *   destinations from its epilogue and combine pass; the sparse variant copies the finished rows
+ *   with one extra kernel.  Ordering: the stores are complete when the stream reaches the next
+ *   operation; making them visible to other GPUs needs the caller's cross-GPU barrier after that.
+ *   Errors: BPS_ERR_INVALID_ARG for ndst outside 0..8, NULL/unaligned destinations or a bad
+ *   ld_dst; otherwise as bps_apply_orbit_range_ws.
+ */
+int bps_apply_orbit_range_bcast(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end,
+                                const void* A_local, int64_t lda, int64_t n, bps_dtype dtype,
+                                float* Y_local, int64_t ldy, float* const* dst, int ndst, float* mc_dst,
+                                int64_t ld_dst, int64_t dst_row0, void* workspace, size_t workspace_bytes,
+                                void* stream, int variant);
+
+/*
  * bps_pattern_host — host evaluation of the frozen pattern draw (R2-R3), for tests:
  *   row ∈ [0, B_r) inside output block g and sign ∈ {+1,-1} of the j-th nonzero of
  *   column u of Φ_{g, f^ℓ(g)} (ell is 1-based). Uses the same code as the device kernels.

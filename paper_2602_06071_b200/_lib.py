@@ -22,7 +22,8 @@ STATUS = {
 EXPORTS = [
     "bps_make_sketch", "bps_free_sketch", "bps_sketch_info", "bps_apply", "bps_apply_t", "bps_apply_ex",
     "bps_apply_t_ex", "bps_workspace_size", "bps_apply_ws", "bps_apply_t_ws", "bps_orbit", "bps_apply_orbit_range",
-    "bps_apply_orbit_range_ws", "bps_orbit_range_workspace_size", "bps_pattern_host", "bps_kernel_launches",
+    "bps_apply_orbit_range_ws", "bps_orbit_range_workspace_size", "bps_apply_orbit_range_bcast", "bps_pattern_host",
+    "bps_kernel_launches",
     "bps_timing_enable", "bps_timing_read", "bps_timing_read_ex",
     "bps_version", "bps_last_error",
 ]
@@ -89,6 +90,11 @@ def _load() -> ctypes.CDLL:
         L.bps_apply_orbit_range_ws.restype = ctypes.c_int
         L.bps_orbit_range_workspace_size.argtypes = [vp, i64, i64, i64, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]
         L.bps_orbit_range_workspace_size.restype = ctypes.c_int
+    if hasattr(L, "bps_apply_orbit_range_bcast"):
+        L.bps_apply_orbit_range_bcast.argtypes = [vp, i64, i64, vp, i64, i64, ctypes.c_int, vp, i64,
+                                                  ctypes.POINTER(vp), ctypes.c_int, vp, i64, i64, vp, ctypes.c_size_t,
+                                                  vp, ctypes.c_int]
+        L.bps_apply_orbit_range_bcast.restype = ctypes.c_int
     L.bps_pattern_host.argtypes = [vp, i64, i32, i64, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.bps_pattern_host.restype = ctypes.c_int
     if hasattr(L, "bps_timing_enable"):  # absent only in old builds loaded via BPS_LIB for A/B runs

@@ -153,8 +153,36 @@ static int dispatch(const bps_sketch* sk, const void* in, int64_t ldin, int64_t 
     // AUTO: a shape the tc planner cannot launch runs on the sparse kernel (bps.h), nothing was enqueued
     if (rc != BPS_ERR_UNSUPPORTED || variant == BPS_VARIANT_TC) return rc;
   }
-  return transposed ? launch_sparse_transposed(sk->p, in, ldin, n, dt, out, ldout, pl, st)
-                    : launch_sparse_rowmajor(sk->p, in, ldin, n, dt, out, ldout, pl, st);
+  if (transposed) return launch_sparse_transposed(sk->p, in, ldin, n, dt, out, ldout, pl, st);
+  rc = launch_sparse_rowmajor(sk->p, in, ldin, n, dt, out, ldout, pl, st);
+  // the CUDA-core kernel has no fused broadcast: copy the finished rows to the destinations
+  if (rc == BPS_OK && pl.bc) rc = launch_bcast_rows(out, ldout, pl.n_out * sk->B_r, n, *pl.bc, st);
+  return rc;
+}
+
+// Unfused broadcast copy: one thread per 4 consecutive elements of a row (row-major).
+__global__ void bps_bcast_rows_kernel(const float* __restrict__ Y, int64_t ldy, int64_t rows, int64_t n,
+                                      const __grid_constant__ Broadcast bc) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, per = (n + 3) / 4;
+  if (q >= rows * per) return;
+  const int64_t r = q / per, c = (q % per) * 4;
+  for (int64_t e = c; e < c + 4 && e < n; ++e) {
+    const float v = Y[r * ldy + e];
+    const int64_t off = (bc.row0 + r) * bc.ld + e;
+    for (int j = 0; j < bc.npeer; ++j) bc.peer[j][off] = v;
+    if (bc.mc) asm volatile("multimem.st.global.f32 [%0], %1;" ::"l"(bc.mc + off), "f"(v) : "memory");
+  }
+}
+
+int launch_bcast_rows(const float* Y, int64_t ldy, int64_t rows, int64_t n, const Broadcast& bc, cudaStream_t st) {
+  const int64_t work = rows * ((n + 3) / 4);
+  if (work <= 0) return BPS_OK;
+  const int64_t blocks = (work + 255) / 256;
+  if (blocks > 0x7FFFFFFF) return fail(BPS_ERR_UNSUPPORTED, "broadcast grid too large");
+  bps_bcast_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(Y, ldy, rows, n, bc);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BPS_OK : fail(BPS_ERR_CUDA, std::string("broadcast launch: ") + cudaGetErrorString(e));
 }
 
 }  // namespace bps
@@ -442,6 +470,33 @@ int bps_apply_orbit_range_ws(const bps_sketch* sk, int64_t pos_begin, int64_t po
   if (workspace && overlaps(workspace, workspace_bytes, Y_local, (size_t)((L * sk->B_r - 1) * ldy + n) * 4))
     return fail(BPS_ERR_INVALID_ARG, "workspace overlaps the output");
   Placement pl{1, pos_begin, L};
+  return dispatch(sk, A_local, lda, n, dtype, Y_local, ldy, false, pl, stream, variant, workspace, workspace_bytes);
+}
+
+int bps_apply_orbit_range_bcast(const bps_sketch* sk, int64_t pos_begin, int64_t pos_end, const void* A_local,
+                                int64_t lda, int64_t n, bps_dtype dtype, float* Y_local, int64_t ldy,
+                                float* const* dst, int ndst, float* mc_dst, int64_t ld_dst, int64_t dst_row0,
+                                void* workspace, size_t workspace_bytes, void* stream, int variant) {
+  int rc = check_range(sk, pos_begin, pos_end);
+  if (rc) return rc;
+  if (ndst < 0 || ndst > 8 || (ndst > 0 && !dst)) return fail(BPS_ERR_INVALID_ARG, "need 0 <= ndst <= 8 destinations");
+  const int64_t L = pos_end - pos_begin;
+  if (ld_dst < n || dst_row0 < 0 || ((ld_dst * 4) % 16)) return fail(BPS_ERR_INVALID_ARG, "bad destination layout");
+  Broadcast bc{};
+  for (int j = 0; j < ndst; ++j) {
+    if (!dst[j] || ((uintptr_t)dst[j] % 16)) return fail(BPS_ERR_INVALID_ARG, "destination pointers must be 16-byte aligned");
+    bc.peer[j] = dst[j];
+  }
+  bc.npeer = ndst;
+  bc.mc = mc_dst;
+  bc.ld = ld_dst;
+  bc.row0 = dst_row0;
+  const int64_t in_rows = (L + sk->kappa - 1) * sk->B_c;
+  rc = validate_apply(sk, A_local, lda, in_rows, n, dtype, Y_local, ldy, L * sk->B_r, n, variant);
+  if (rc || n == 0) return rc;
+  if (workspace && overlaps(workspace, workspace_bytes, Y_local, (size_t)((L * sk->B_r - 1) * ldy + n) * 4))
+    return fail(BPS_ERR_INVALID_ARG, "workspace overlaps the output");
+  Placement pl{1, pos_begin, L, (ndst > 0 || mc_dst) ? &bc : nullptr};
   return dispatch(sk, A_local, lda, n, dtype, Y_local, ldy, false, pl, stream, variant, workspace, workspace_bytes);
 }
 

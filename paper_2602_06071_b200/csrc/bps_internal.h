@@ -31,11 +31,24 @@ int fail(int code, const std::string& msg);
 //   full mode : o = g;  input block for ℓ at row f^ℓ(g)·B_c;  output rows g·B_r.
 //   range mode: o = local orbit index; g = f^(pos_begin+o)(0); input block for ℓ at local
 //               stacked block o+ℓ-1; output rows o·B_r.
+// Output broadcast of an orbit-range apply (bps_apply_orbit_range_bcast): every final element of Y
+// row r is also stored to row row0 + r of each destination (and through the NVLS multicast address).
+struct Broadcast {
+  float* peer[8];
+  int npeer;
+  float* mc;
+  int64_t ld, row0;
+};
+
 struct Placement {
   int range_mode;
   int64_t pos_begin;
   int64_t n_out;  // number of output blocks launched (grid.x)
+  const Broadcast* bc = nullptr;  // row-major orbit ranges only
 };
+
+// Unfused broadcast (sparse variant): copy rows [0, rows) of Y to every destination of bc.
+int launch_bcast_rows(const float* Y, int64_t ldy, int64_t rows, int64_t n, const Broadcast& bc, cudaStream_t st);
 
 // Sparse CUDA-core kernels (bps_sparse.cu).
 int launch_sparse_rowmajor(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt,

@@ -53,6 +53,7 @@ namespace {
 
 constexpr int kBandTile = 128 * kBK * 2;  // one M-tile (128 band rows) of a band stage, bytes
 constexpr int kMaxRanges = 511;           // canon: stream ranges per column tile (TcArgs::rb)
+constexpr int kMaxPeers = 8;              // output broadcast destinations (TcArgs::peer)
 
 // Warp roles (the issue arbiter favours high warp ids, so the latency-critical single-thread
 // roles take the last two warps): 0-3 epilogue (TMEM lane quarters 0-3) | 4-11 band
@@ -184,7 +185,34 @@ struct TcArgs {
             // 8 cycle trace, 16 no band proxy fence, 32 band without hashing,
             // 64 (with 4) ring slots released by thread arrives instead of tcgen05.commit
   unsigned long long* trace;   // dbg & 8: per-CTA cycle counters (16 per CTA), else nullptr
+  // output broadcast (row-major orbit ranges; bps_apply_orbit_range_bcast): every FINAL
+  // element of Y row r is also stored to row prow0 + r of the npeer destination buffers (peer or
+  // local device pointers) and, when mc is set, through the NVLS multicast address mc (multimem.st,
+  // one store reaching every GPU bound to it) — the all-gather of block sharding, fused into the
+  // epilogue.  Parked prefixes (canon) stay in Y only.
+  float* peer[kMaxPeers];
+  int npeer;
+  float* mc;
+  int64_t ldp, prow0;
 };
+
+// broadcast of one final element / four consecutive ones (row-major)
+__device__ __forceinline__ void bcast1(const TcArgs& a, int64_t row, int64_t col, float v) {
+  const int64_t off = (a.prow0 + row) * a.ldp + col;
+  for (int j = 0; j < a.npeer; ++j) a.peer[j][off] = v;
+  if (a.mc) asm volatile("multimem.st.global.f32 [%0], %1;" ::"l"(a.mc + off), "f"(v) : "memory");
+}
+__device__ __forceinline__ void bcast4(const TcArgs& a, int64_t row, int64_t col, float4 v) {
+  const int64_t off = (a.prow0 + row) * a.ldp + col;
+  if (off & 3) {  // ldp not a multiple of 4: scalar stores
+    bcast1(a, row, col, v.x), bcast1(a, row, col + 1, v.y), bcast1(a, row, col + 2, v.z), bcast1(a, row, col + 3, v.w);
+    return;
+  }
+  for (int j = 0; j < a.npeer; ++j) *reinterpret_cast<float4*>(a.peer[j] + off) = v;
+  if (a.mc)
+    asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a.mc + off), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
 
 // Geometry of the canonical stream decomposition (canon mode), shared by bps_tc_kernel (tile
 // addresses) and bps_tc_combine (which folds the tiles of a straddling output in stream order).
@@ -728,10 +756,12 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
             for (int r = 0; r < Br; ++r) {
               const float v = exact_elem<F32, TRANS>(args, i, (uint32_t)r, col, et, fixred);
               if (et == 0) {
-                if (!TRANS)
+                if (!TRANS) {
                   args.Y[(yr0 + r) * args.ldy + col] = v;
-                else
+                  if (args.npeer || args.mc) bcast1(args, yr0 + r, col, v);
+                } else {
                   args.Y[col * args.ldy + yr0 + r] = v;
+                }
               }
             }
           }
@@ -757,13 +787,19 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         bool bad = false;
         if (!TRANS) {
           float* y = args.Y + yrow * args.ldy + cb;
+          const bool bc = args.npeer || args.mc;
 #pragma unroll
           for (int t = 0; t < 16; t += 4) {
             if (cb + t + 3 < args.n) {
-              *reinterpret_cast<float4*>(y + t) = make_float4(v[t], v[t + 1], v[t + 2], v[t + 3]);
+              const float4 q4 = make_float4(v[t], v[t + 1], v[t + 2], v[t + 3]);
+              *reinterpret_cast<float4*>(y + t) = q4;
+              if (bc) bcast4(args, yrow, cb + t, q4);
             } else {
               for (int e = 0; e < 4; ++e)
-                if (cb + t + e < args.n) y[t + e] = v[t + e];
+                if (cb + t + e < args.n) {
+                  y[t + e] = v[t + e];
+                  if (bc) bcast1(args, yrow, cb + t + e, v[t + e]);
+                }
             }
           }
         } else {
@@ -782,10 +818,12 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         if (cb >= args.n) return false;
         bool bad = false;
         float* y = args.Y + yrow0 * args.ldy + cb;
+        const bool bc = args.npeer || args.mc;
 #pragma unroll
         for (int t = 0; t < 16; ++t)
           if (t >= t0 && t < t1) {
             y[(int64_t)t * args.ldy] = v[t];
+            if (bc) bcast1(args, yrow0 + t, cb, v[t]);
             bad |= needs_exact(v[t]);
           }
         if (bad) mark_bad(cl);
@@ -1505,6 +1543,10 @@ __global__ void __launch_bounds__(256) bps_tc_combine(const __grid_constant__ Tc
       if (yo[k] >= 0) {
         const float v = acc[k] * p.scale;
         Yb[yo[k]] = v;
+        if (!TRANS && (args.npeer || args.mc)) {
+          const int e = e0 + k * NT;
+          bcast1(args, yr0 + (TF ? e / BN : e % Br), col0 + (TF ? e % BN : e / Br), v);
+        }
         const uint32_t bits = __float_as_uint(v), ex = (bits >> 23) & 0xFFu;
         if (ex == 0xFFu || (ex < 27u && (bits & 0x7FFFFFFFu) != 0u)) {  // see needs_exact
           bad = true;
@@ -1523,10 +1565,12 @@ __global__ void __launch_bounds__(256) bps_tc_combine(const __grid_constant__ Tc
       for (int r = 0; r < Br; ++r) {
         const float v = exact_elem<F32, TRANS>(args, i, (uint32_t)r, col, (int)threadIdx.x, red);
         if (threadIdx.x == 0) {
-          if (!TRANS)
+          if (!TRANS) {
             args.Y[(yr0 + r) * args.ldy + col] = v;
-          else
+            if (args.npeer || args.mc) bcast1(args, yr0 + r, col, v);
+          } else {
             args.Y[col * args.ldy + yr0 + r] = v;
+          }
         }
       }
     }
@@ -1655,6 +1699,13 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
   if (a.canon && R > kMaxRanges) R = kMaxRanges;
   a.R = (int)R;
   a.nct = (int)n_ct;
+  if (pl.bc) {  // fused output broadcast (row-major orbit ranges; the host rejects the transposed layout)
+    for (int j = 0; j < pl.bc->npeer; ++j) a.peer[j] = pl.bc->peer[j];
+    a.npeer = pl.bc->npeer;
+    a.mc = pl.bc->mc;
+    a.ldp = pl.bc->ld;
+    a.prow0 = pl.bc->row0;
+  }
   if (a.canon) {
     const int64_t NGt = a.stream_len * nk / hp.G;
     for (int64_t r = 0; r <= R; ++r) a.rb[r] = (int)(hp.G * (NGt * r / R));

@@ -93,3 +93,58 @@ def block_sharded_apply(sk, A_local, group=None, apply_range: Callable | None = 
         out.copy_(Y)
         return out
     return Y
+
+
+def symmetric_rendezvous(shape, device, group=None):
+    """Allocate a symmetric fp32 buffer on every rank of `group` (torch symmetric memory) and return
+    (buffer, peer pointers (one per rank, valid in this process), multicast address or 0, barrier)."""
+    import torch
+    import torch.distributed._symmetric_memory as symm_mem
+
+    buf = symm_mem.empty(shape, dtype=torch.float32, device=device)
+    hdl = symm_mem.rendezvous(buf, group if group is not None else _default_group_name())
+    ptrs = [int(p) for p in hdl.buffer_ptrs]
+    mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
+    return buf, ptrs, mc, lambda: hdl.barrier(channel=0)
+
+
+def _default_group_name():
+    import torch.distributed as dist
+
+    return dist.group.WORLD.group_name
+
+
+def block_sharded_apply_fused(sk, A_local, group=None, rendezvous: Callable | None = None,
+                              apply_range: Callable | None = None, multicast: bool = True, variant: str = "auto"):
+    """Orbit block-sharded Y = S·A with the all-gather fused into the kernel epilogue (SURVEY §8(e)
+    B200-native step): rank r's kernel stores each finished output tile of its orbit
+    positions [p0, p1) straight into EVERY rank's symmetric orbit-ordered Y buffer — one multimem.st
+    through the NVLS multicast address when the symmetric-memory handle exposes one, else one store
+    per peer pointer over NVLink (bps_apply_orbit_range_bcast) — then one cross-GPU barrier; no
+    separate collective pass.  Returns the full k×n Y (g order) on every rank, bitwise equal to
+    block_sharded_apply and to the 1-GPU apply (R19).
+
+    rendezvous(shape, device, group) -> (buffer, peer_ptrs, mc_ptr, barrier) and
+    apply_range(p0, p1, A_local, dst_ptrs, mc_ptr, dst_row0) are injectable for the CPU (gloo) tests.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    M, B_r = sk.M, sk.B_r
+    p0, p1 = orbit_shard(M, world, rank)
+    n = A_local.shape[1]
+    rv = rendezvous or symmetric_rendezvous
+    Y_orbit, ptrs, mc, barrier = rv((M * B_r, n), A_local.device, group)
+    if not (multicast and mc):
+        mc = 0
+    dst = () if mc else tuple(ptrs)
+    if apply_range is None:
+        sk.apply_orbit_range(p0, p1, A_local, variant=variant, dst=dst, mc_ptr=mc, dst_ld=Y_orbit.stride(0),
+                             dst_row0=p0 * B_r)
+    else:
+        apply_range(p0, p1, A_local, dst, mc, p0 * B_r)
+    barrier()  # every rank's stores have landed in every buffer
+    orbit = sk.orbit() if hasattr(sk, "orbit") else sk["orbit"]
+    return gather_orbit_to_g(Y_orbit, orbit, B_r)

@@ -195,9 +195,14 @@ class Sketch:
         return out
 
     def apply_orbit_range(self, pos_begin: int, pos_end: int, A_local, out=None, variant: str = "auto",
-                          use_workspace: bool = True):
+                          use_workspace: bool = True, dst=(), mc_ptr: int = 0, dst_ld: int | None = None,
+                          dst_row0: int = 0):
         """Partial apply over orbit positions [pos_begin, pos_end) (bps_apply_orbit_range_ws): the
-        output blocks at those positions, stacked, bitwise equal to the matching rows of apply()."""
+        output blocks at those positions, stacked, bitwise equal to the matching rows of apply().
+
+        dst / mc_ptr (bps_apply_orbit_range_bcast): the kernel epilogue also stores every output row r
+        into row dst_row0 + r of each destination — device pointers (ints: peers' symmetric buffers
+        or local tensors' data_ptr()) and/or an NVLS multicast address — with leading dimension dst_ld."""
         import torch
 
         _check_matrix(A_local, "A_local")
@@ -217,6 +222,17 @@ class Sketch:
             check(lib.bps_orbit_range_workspace_size(self._h, pos_begin, pos_end, n, code, ctypes.byref(b)))
             nbytes = b.value
         ws, wsb = self._scratch(nbytes, A_local.device)
+        if dst or mc_ptr:
+            ptrs = [int(p) for p in dst]
+            if len(ptrs) > 8:
+                raise ValueError("at most 8 destinations")
+            arr = (ctypes.c_void_p * max(1, len(ptrs)))(*ptrs)
+            check(lib.bps_apply_orbit_range_bcast(self._h, pos_begin, pos_end, A_local.data_ptr(), A_local.stride(0), n,
+                                                  code, out.data_ptr(), out.stride(0), arr, len(ptrs), mc_ptr or None,
+                                                  dst_ld if dst_ld is not None else n, dst_row0,
+                                                  ws.data_ptr() if ws is not None else None, wsb,
+                                                  _stream_ptr(A_local.device), VARIANTS[variant]))
+            return out
         check(lib.bps_apply_orbit_range_ws(self._h, pos_begin, pos_end, A_local.data_ptr(), A_local.stride(0), n, code,
                                            out.data_ptr(), out.stride(0), ws.data_ptr() if ws is not None else None,
                                            wsb, _stream_ptr(A_local.device), VARIANTS[variant]))

@@ -109,3 +109,65 @@ def test_block_sharded_apply_gloo(world):
         assert p.exitcode == 0
     for rank, err in res:
         assert err < 1e-12, (rank, err)
+
+
+class _FakeSymmetric:
+    """Emulates torch symmetric memory for the CPU test: 'peer pointers' are rank ids; the stores a
+    rank's kernel would make into every peer's buffer are replayed at the barrier through gloo."""
+
+    def __init__(self, sk):
+        self.sk = sk
+        self.pending = []
+
+    def rendezvous(self, shape, device, group):
+        self.world = dist.get_world_size(group)
+        self.buf = torch.full(shape, float("nan"), dtype=torch.float64)
+        return self.buf, list(range(self.world)), 0, self.barrier
+
+    def apply_range(self, p0, p1, A_local, dst, mc, row0):
+        assert tuple(dst) == tuple(range(self.world)) and mc == 0
+        self.pending.append((row0, self.sk.apply_range(p0, p1, A_local)))
+
+    def barrier(self):
+        got = [None] * self.world
+        dist.all_gather_object(got, self.pending)
+        for lst in got:
+            for row0, Y in lst:
+                self.buf[row0:row0 + Y.shape[0]] = Y
+
+
+def _worker_fused(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        osk = oracle.make_sketch(8, 32, 128, 2, 2, 1234)
+        sk = _OracleRanks(osk)
+        rng = np.random.default_rng(8)
+        A = rng.standard_normal((osk.d, 5))
+        p0, p1 = D.orbit_shard(osk.M, world, rank)
+        blocks = D.input_blocks(sk.orbit(), p0, p1, osk.kappa)
+        A_local = torch.from_numpy(np.concatenate([A[h * osk.B_c:(h + 1) * osk.B_c] for h in blocks]))
+        fake = _FakeSymmetric(sk)
+        Y = D.block_sharded_apply_fused(sk, A_local, rendezvous=fake.rendezvous, apply_range=fake.apply_range)
+        ref = oracle.apply(osk, A)
+        out_q.put((rank, float(np.abs(Y.numpy() - ref).max())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_block_sharded_apply_fused_gloo():
+    """Host logic of the fused (epilogue-broadcast) block sharding: destination rows p0·B_r.. of every
+    rank's orbit-ordered buffer, one barrier, orbit→g permutation — world 2 on CPU."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_fused, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    for rank, err in res:
+        assert err < 1e-12, (rank, err)

@@ -199,3 +199,87 @@ def test_workspace_epochs(variant):
     for _ in range(3):
         for n in (384, 64):
             assert torch.equal(sk.apply(A[:, :n].contiguous(), variant=variant), ref[n])
+
+
+BCAST_CASES = [CASES[0], CASES[1], CASES[2], CASES[3], CASES[7], CASES[8]]
+
+
+@pytest.mark.parametrize("case", BCAST_CASES, ids=[f"{c[0]}-n{c[1]}-{c[2]}-{c[3]}" for c in BCAST_CASES])
+@pytest.mark.parametrize("variant", ["tc", "sparse"])
+@pytest.mark.parametrize("use_ws", [True, False])
+def test_orbit_range_bcast(case, variant, use_ws):
+    """bps_apply_orbit_range_bcast (the all-gather fused into the epilogue): three
+    destination buffers with a padded leading dimension stand in for the peers' symmetric buffers;
+    each receives, at rows dst_row0.., bitwise the rows of Y_local (= the full apply's rows), and
+    nothing outside them."""
+    layout, n, dt, mode = case
+    sk = Sketch(*layout, seed=36, mode=mode)
+    M = sk.M
+    A = torch.randn((sk.d, n), device="cuda").to(_tdt(dt))
+    try:
+        Y = sk.apply(A, variant=variant)
+    except BpsError as e:
+        if e.code == -3 and variant == "tc":
+            pytest.skip(str(e))
+        raise
+    orb = sk.orbit()
+    ld = n + 4
+    for p0, p1 in sorted({(0, M), (M - 1, M + min(2, M - 1)), (1, 1 + max(1, M // 2))}):
+        if p1 <= p0:
+            continue
+        rows = (p1 - p0) * sk.B_r
+        row0 = (p0 % 3) * sk.B_r + 5
+        dsts = [torch.full((row0 + rows + 7, ld), float("nan"), device="cuda") for _ in range(3)]
+        Yl = sk.apply_orbit_range(p0, p1, _orbit_local(sk, A, p0, p1), variant=variant, use_workspace=use_ws,
+                                  dst=[t.data_ptr() for t in dsts], dst_ld=ld, dst_row0=row0)
+        torch.cuda.synchronize()
+        ref = torch.cat([Y[orb[p % M] * sk.B_r:(orb[p % M] + 1) * sk.B_r] for p in range(p0, p1)])
+        assert torch.equal(Yl, ref), (p0, p1)
+        for t in dsts:
+            assert torch.equal(t[row0:row0 + rows, :n], Yl), (p0, p1)
+            assert torch.isnan(t[:row0]).all() and torch.isnan(t[row0 + rows:]).all() and torch.isnan(t[:, n:]).all()
+
+
+def test_orbit_range_bcast_nonfinite():
+    """The exact-recompute path (R12) also reaches the destinations."""
+    sk = Sketch(16, 32, 1024, 4, 4, seed=37)
+    A = torch.randn((sk.d, 128), device="cuda")
+    A[5, 3] = float("inf")
+    A[700, 9] = float("nan")
+    Y = sk.apply(A)
+    M = sk.M
+    dst = torch.full((M * sk.B_r, 128), 7.0, device="cuda")
+    Yl = sk.apply_orbit_range(0, M, _orbit_local(sk, A, 0, M), dst=[dst.data_ptr()], dst_ld=128, dst_row0=0)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.nan_to_num(Yl, nan=1.5), torch.nan_to_num(dst, nan=1.5))
+    orb = sk.orbit()
+    ref = torch.cat([Y[orb[p] * sk.B_r:(orb[p] + 1) * sk.B_r] for p in range(M)])
+    assert torch.equal(torch.nan_to_num(Yl, nan=1.5), torch.nan_to_num(ref, nan=1.5))
+
+
+def test_block_sharded_apply_fused_nccl_world1():
+    """dist.block_sharded_apply_fused through a real NCCL group (world 1) and torch symmetric memory:
+    the epilogue stores straight into the symmetric buffer (peer pointer, and the NVLS multicast
+    address when the platform exposes one); bitwise equal to the full apply."""
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        sk = Sketch(64, 16, 2048, 8, 2, seed=38)
+        A = torch.randn((sk.d, 256), device="cuda", dtype=torch.bfloat16)
+        p0, p1 = D.orbit_shard(sk.M, 1, 0)
+        blocks = D.input_blocks(sk.orbit(), p0, p1, sk.kappa)
+        A_loc = torch.cat([A[h * sk.B_c:(h + 1) * sk.B_c] for h in blocks])
+        ref = sk.apply(A)
+        try:
+            D.symmetric_rendezvous((8, 8), A.device)
+        except Exception as e:  # noqa: BLE001 — platform without symmetric memory
+            pytest.skip(f"torch symmetric memory unavailable: {e}")
+        for mc in (False, True):
+            Y = D.block_sharded_apply_fused(sk, A_loc, multicast=mc)
+            torch.cuda.synchronize()
+            assert torch.equal(Y, ref), f"multicast={mc}"
+    finally:
+        dist.destroy_process_group()
