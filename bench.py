@@ -39,11 +39,12 @@ def parse():
     ap.add_argument("--config", default="ls")
     ap.add_argument("--variant", default="auto", choices=["auto", "sparse", "tc"])
     ap.add_argument("--kind", default="gaussian", choices=["gaussian", "coherent", "lowrank"])
-    ap.add_argument("--shard", default="column", choices=["column", "block"],
+    ap.add_argument("--shard", default="column", choices=["column", "block", "block-fused"],
                     help="column: weak scaling, every rank its own n-column batch (no collective; at N>1 the "
                          "line also carries the strong-scaling measurement: the config's n split over the "
                          "ranks with dist.column_shard); block: strong scaling of one d×n problem sharded along "
-                         "the wiring orbit + all-gather")
+                         "the wiring orbit + all-gather; block-fused: the same with the all-gather fused into the "
+                         "kernel epilogue (stores into the peers' symmetric buffers, dist.block_sharded_apply_fused)")
     ap.add_argument("--op", default="apply", choices=["apply", "adjoint"],
                     help="adjoint: X = Sᵀ·Y (fp32 k×n -> d×n) on the same sketch; secondary line, no e2e/cpu legs")
     ap.add_argument("--sketch", default="blockperm", choices=["blockperm", "blockrow"],
@@ -301,7 +302,7 @@ def main():
     if args.sketch == "blockrow":  # secondary line: the e2e/cpu legs are defined for the main sketch
         args.no_cpu_baseline = args.no_e2e = True
     stream = torch.cuda.current_stream(dev)
-    if args.shard == "block" and world > 1:
+    if args.shard in ("block", "block-fused") and world > 1:
         from paper_2602_06071_b200 import dist as D
 
         p0, p1 = D.orbit_shard(cfg.M, world, rank)
@@ -311,7 +312,10 @@ def main():
         Y = torch.empty((cfg.k, n), dtype=torch.float32, device=dev)
 
         def step():
-            D.block_sharded_apply(sk, A, out=Y)
+            if args.shard == "block-fused":
+                Y.copy_(D.block_sharded_apply_fused(sk, A, variant=args.variant))
+            else:
+                D.block_sharded_apply(sk, A, out=Y)
     elif args.op == "adjoint":
         Yin = synth.device_matrix(args.kind, cfg.k, n, seed=1000 + rank, dtype=torch.float32, device=dev)
         X = torch.empty((cfg.d, n), dtype=torch.float32, device=dev)
@@ -401,7 +405,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_max = float(t.item())
     ms = total_max / args.steps
-    block = args.shard == "block" and world > 1
+    block = args.shard in ("block", "block-fused") and world > 1
     bytes_rank = cfg.roofline_bytes(n) if not block else cfg.roofline_bytes(n) // world
     if args.op == "adjoint":  # read Y (k×n fp32) once, write X (d×n fp32) once
         bytes_rank = (cfg.k + cfg.d) * n * 4
@@ -505,7 +509,8 @@ def main():
             "data": f"synthetic {args.kind} (torch Philox on device), seed {1000}+rank",
             "config": {"workload": cfg.name, "d": cfg.d, "k": cfg.k, "kappa": cfg.kappa, "s": cfg.s,
                        "n_per_gpu": n, "B_r": cfg.B_r, "M": cfg.M, "B_c": cfg.B_c, "variant": args.variant, "op": args.op, "sketch": args.sketch, "mode": args.mode, "layout": args.layout,
-                       "parallelism": (f"orbit-block-shard x{world} + NCCL all_gather" if block
+                       "parallelism": (f"orbit-block-shard x{world} + " + ("epilogue broadcast into symmetric memory"
+                                       if args.shard == "block-fused" else "NCCL all_gather") if block
                                        else f"column-shard x{world} (no collective)"),
                        "l2": "inputs larger than L2 (no flush needed)" if bytes_rank > (256 << 20) else "input fits L2"},
             "columns_per_s": (n if block else world * n) / (ms / 1e3),

@@ -101,11 +101,18 @@ def symmetric_rendezvous(shape, device, group=None):
     import torch
     import torch.distributed._symmetric_memory as symm_mem
 
+    key = (tuple(shape), str(device), group if isinstance(group, str) else id(group))
+    if key in _SYMM:  # one symmetric buffer per (shape, device, group), reused across calls
+        return _SYMM[key]
     buf = symm_mem.empty(shape, dtype=torch.float32, device=device)
     hdl = symm_mem.rendezvous(buf, group if group is not None else _default_group_name())
     ptrs = [int(p) for p in hdl.buffer_ptrs]
     mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
-    return buf, ptrs, mc, lambda: hdl.barrier(channel=0)
+    _SYMM[key] = (buf, ptrs, mc, lambda: hdl.barrier(channel=0))
+    return _SYMM[key]
+
+
+_SYMM: dict = {}
 
 
 def _default_group_name():
