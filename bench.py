@@ -76,6 +76,16 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def measured_tensor_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        if "bf16_tflops" in d:
+            return float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, dense burst)"
+    return 2250.0, "nominal (B200 dense bf16)"
+
+
 def ncu_traffic(cfg_name, variant):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
@@ -420,6 +430,20 @@ def main():
     else:
         achieved = bytes_rank / ((kern_ms if kern_ms else statistics.mean(per)) / 1e3) / 1e9
 
+    # the dense ±1 band costs 2·κ·B_r flops per input element (×2 for the fp32 hi/lo split): where that
+    # needs more time at the measured tensor peak than the bytes at the HBM peak, the kernel's roofline
+    # is the tensor pipe (the κ·B_r = 512 sweep points)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak}
+    if args.op == "apply" and args.sketch == "blockperm" and args.variant != "sparse" and not block:
+        tpeak, tsrc = measured_tensor_peak()
+        flops = 2.0 * cfg.kappa * cfg.B_r * cfg.d * n * (2 if cfg.dtype == "f32" else 1)
+        if flops / (tpeak * 1e12) > bytes_rank / (peak * 1e9):
+            t_launch = (kern_ms if kern_ms else statistics.mean(per)) / 1e3
+            ach_t = flops / (launches_per_step or 1) / t_launch / 1e12
+            roof = {"bound": "tensor", "achieved": ach_t, "peak": tpeak, "unit": "TFLOP/s", "frac": ach_t / tpeak,
+                    "flops_per_launch": flops / (launches_per_step or 1), "tensor_peak_source": tsrc,
+                    "hbm": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak}}
+
     # strong scaling (column mode, N > 1): the config's n columns split over the ranks (tile-aligned,
     # dist.column_shard), max-over-ranks device time, value = the whole job's bytes / that time
     strong = None
@@ -518,7 +542,7 @@ def main():
             "gbs_per_gpu": value / world,
             "frac_of_8tbs": value / world / 8000.0,
             "ms_min": min(per), "ms_median": statistics.median(per),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "roofline": {**roof,
                          "traffic": ncu_traffic(cfg.name + (":t" if args.layout == "t" else "") + (":affine" if args.mode == "affine" else ""),
                                                 args.variant) if (args.op == "apply" and args.sketch == "blockperm") else None,
                          "peak_source": peak_src,
