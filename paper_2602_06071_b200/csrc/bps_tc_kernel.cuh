@@ -180,7 +180,7 @@ struct TcArgs {
   int ab;                      // A/B knob (env BPS_TC_AB): 2 skip contributor tile writes (results
                                // wrong), 4 evict_normal for partials, 8 combine with 128 threads,
                                // 16 combine without programmatic dependent launch, 32 skip the main kernel,
-                               // 64 combine element parts not capped at one wave
+                               // 64 combine element parts not capped at one wave, 128 early PDL trigger
   int dbg;  // experiment switches (env BPS_TC_DEBUG; 0 in production): 1 no band, 2 no convert, 4 no MMA,
             // 8 cycle trace, 16 no band proxy fence, 32 band without hashing,
             // 64 (with 4) ring slots released by thread arrives instead of tcgen05.commit
@@ -488,6 +488,10 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
   else
     __syncthreads();
   ptx::tc_fence_after();
+  // programmatic dependent launch, early trigger (BPS_TC_AB & 128, experiment): the combine pass may
+  // be scheduled once every CTA of this grid has started, its CTAs waiting in griddepcontrol.wait
+  // on SMs freed by finished ranges — measured 1-2 % slower on LS than the trigger at CTA end
+  if (args.ab & 128) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t tmem = *tmem_ptr;               // D: per-group tensor-core accumulator
   const uint32_t tmem_S = tmem + NMT * K::DN;    // S: fp32 running sums (RN adds on CUDA cores)
   const uint32_t tmem_A = tmem + K::OFF_TA;      // TF: A operand stages (data hi | lo)
@@ -1457,7 +1461,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
   }
   // this CTA's stores are issued: let the combine kernel (programmatic dependent launch) start its
   // prologue; it reads our data only after griddepcontrol.wait (full completion of this grid)
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (!(args.ab & 128)) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 
