@@ -185,7 +185,8 @@ size_t workspace_impl(const SketchParams& p, int64_t n, bps_dtype dt, bool trans
   const Choice c = choose(p, n, dt, transposed, pl, cv.nmt, cv.ss, sms, true, G);
   const int64_t nct = (n + c.bn - 1) / c.bn;
   const int64_t ctas = std::max<int64_t>(nct, sms);  // grid = nct·R ≤ max(nct, co-resident slots)
-  return (size_t)ctas * (size_t)tiles_per_cta(p, G) * p.B_r * c.bn * 4;
+  // partial tiles + one 8-byte publication flag per CTA (slot-split clusters: ss CTAs per tile)
+  return (size_t)ctas * (size_t)tiles_per_cta(p, G) * p.B_r * c.bn * 4 + (size_t)ctas * c.ss * 8;
 }
 
 int launch_tc_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, bps_dtype dt, float* Y, int64_t ldy,

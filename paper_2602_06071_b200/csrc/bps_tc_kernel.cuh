@@ -38,7 +38,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdio>
+#include <random>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
@@ -180,7 +183,8 @@ struct TcArgs {
   int ab;                      // A/B knob (env BPS_TC_AB): 2 skip contributor tile writes (results
                                // wrong), 4 evict_normal for partials, 8 combine with 128 threads,
                                // 16 combine without programmatic dependent launch, 32 skip the main kernel,
-                               // 64 combine element parts not capped at one wave, 128 early PDL trigger
+                               // 64 combine element parts not capped at one wave, 128 swap the PDL
+                               // trigger position, 256 per-CTA flags (combine does not wait for the grid)
   int dbg;  // experiment switches (env BPS_TC_DEBUG; 0 in production): 1 no band, 2 no convert, 4 no MMA,
             // 8 cycle trace, 16 no band proxy fence, 32 band without hashing,
             // 64 (with 4) ring slots released by thread arrives instead of tcgen05.commit
@@ -190,6 +194,13 @@ struct TcArgs {
   // local device pointers) and, when mc is set, through the NVLS multicast address mc (multimem.st,
   // one store reaching every GPU bound to it) — the all-gather of block sharding, fused into the
   // epilogue.  Parked prefixes (canon) stay in Y only.
+  // canon handoff to bps_tc_combine without waiting for the whole grid: CTA b publishes
+  // flags[b] = epoch (release) once its partial tiles and parked prefixes are stored; the combine
+  // pass acquires the flags of exactly the CTAs an output needs.  epoch is unique per launch, so the
+  // workspace needs no initialisation.  flags == nullptr: griddepcontrol.wait (whole grid)
+  unsigned long long* flags;
+  unsigned long long epoch;
+  int ss;                      // slot-split CTAs per (range, column tile)
   float* peer[kMaxPeers];
   int npeer;
   float* mc;
@@ -488,10 +499,13 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
   else
     __syncthreads();
   ptx::tc_fence_after();
-  // programmatic dependent launch, early trigger (BPS_TC_AB & 128, experiment): the combine pass may
-  // be scheduled once every CTA of this grid has started, its CTAs waiting in griddepcontrol.wait
-  // on SMs freed by finished ranges — measured 1-2 % slower on LS than the trigger at CTA end
-  if (args.ab & 128) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // programmatic dependent launch: with the flag handoff the combine pass is triggered as soon as
+  // every CTA of this grid has started — its CTAs take SMs freed by finished ranges and fold each
+  // straddling output as soon as the CTAs holding its pieces have published them, inside this
+  // kernel's tail.  Without flags the trigger sits at the CTA end (BPS_TC_AB & 128 swaps both:
+  // early with griddepcontrol.wait measured 1-2 % slower on LS)
+  const bool early_trigger = args.flags ? !(args.ab & 128) : (args.ab & 128) != 0;
+  if (early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t tmem = *tmem_ptr;               // D: per-group tensor-core accumulator
   const uint32_t tmem_S = tmem + NMT * K::DN;    // S: fp32 running sums (RN adds on CUDA cores)
   const uint32_t tmem_A = tmem + K::OFF_TA;      // TF: A operand stages (data hi | lo)
@@ -1010,6 +1024,13 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
             }
           }
         }
+        if (args.flags) {
+          // every tile and prefix of this CTA is stored: publish them (gpu-scope release)
+          __threadfence();
+          ptx::named_bar_sync(kEpiBar, 128);
+          if (et == 0)
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(args.flags + blockIdx.x), "l"(args.epoch) : "memory");
+        }
       }
     } else if (warp >= 4 && warp < 4 + K::NBW) {
       // the intra-block mode is a launch constant: specialise the whole generator on it
@@ -1447,6 +1468,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
       tr.add(12, tstart);
     }
   }
+  if (args.flags && S1 <= S0 && threadIdx.x == 0)  // an empty range has nothing to publish
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(args.flags + blockIdx.x), "l"(args.epoch) : "memory");
   const unsigned long long t_end0 = tr_cta.now();
   ptx::tc_fence_before();
   if (K::CL > 1)
@@ -1461,7 +1484,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
   }
   // this CTA's stores are issued: let the combine kernel (programmatic dependent launch) start its
   // prologue; it reads our data only after griddepcontrol.wait (full completion of this grid)
-  if (!(args.ab & 128)) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (!early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 
@@ -1495,18 +1518,39 @@ __global__ void __launch_bounds__(256) bps_tc_combine(const __grid_constant__ Tc
   if (threadIdx.x < 8) fixmap[threadIdx.x] = 0u;
   __syncthreads();
   geo.rb = srb;
-  if (F + geo.KN <= geo.range_begin(geo.range_of(F) + 1)) return;  // finished by its owner
+  if (F + geo.KN <= geo.range_begin(geo.range_of(F) + 1)) {  // finished by its owner
+    // with flags, one CTA still orders this grid's completion after the stream kernel's
+    if (args.flags && blockIdx.x == 0 && blockIdx.y == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
+  // flags: the CTA holding output i's slot in range r is (r·nct + ct)·ss + slot / (κ/ss)
+  const int css_i = args.ss > 1 ? (int)((uint32_t)(i % (int)p.kappa + (int)p.kappa) % p.kappa) / ((int)p.kappa / args.ss) : 0;
+  auto acquire = [&](int r_) {  // spin until CTA (r_, ct) published this launch's epoch
+    const unsigned long long* f = args.flags + ((int64_t)r_ * args.nct + ct) * args.ss + css_i;
+    unsigned long long v, t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v == args.epoch) break;
+      __nanosleep(256);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 60000000000ull) __trap();  // 60 s: a lost flag is a bug, fail loudly instead of hanging
+    }
+  };
   if (threadIdx.x == 0) {
     int nt = 0;
+    if (args.flags) acquire(geo.range_of(F));  // the owner's parked prefix
     geo.walk(i, [&](int r_, int j, int ngr) {
+      if (args.flags && ngr > 0) acquire(r_);
       for (int g = 0; g < ngr; ++g) tiles[nt++] = geo.tile(r_, ct, j, g);
     });
     ntiles = nt;
   }
+  // without flags: programmatic dependent launch — everything above ran while bps_tc_kernel was
+  // finishing; its prefixes and partial tiles are visible after this wait
+  if (!args.flags) asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
-  // programmatic dependent launch: everything above ran while bps_tc_kernel was finishing; its
-  // prefixes and partial tiles are visible after this wait
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int nt = ntiles, NT = (int)blockDim.x, Br = geo.Br;
   const int el0 = (int)((int64_t)Br * BN * part / nsplit), nel = (int)((int64_t)Br * BN * (part + 1) / nsplit);
   const int64_t col0 = (int64_t)ct * BN;
@@ -1559,6 +1603,9 @@ __global__ void __launch_bounds__(256) bps_tc_combine(const __grid_constant__ Tc
         }
       }
   }
+  // with flags this grid may overtake the stream kernel's teardown: complete only after it, so that
+  // work queued after this apply observes both grids finished
+  if (args.flags) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (!__syncthreads_or(bad) || threadIdx.x >= 128) return;  // warps 0-3 recompute (exact_elem: 128 threads)
   for (int w = 0; w < BN / 32; ++w) {
     uint32_t bits = fixmap[w];
@@ -1582,6 +1629,18 @@ __global__ void __launch_bounds__(256) bps_tc_combine(const __grid_constant__ Tc
 }
 
 }  // namespace
+
+// A value no earlier launch in this process wrote into any workspace flag, and that stale or
+// uninitialised workspace contents match only with probability 2^-64 (random 32-bit salt per process).
+inline unsigned long long next_epoch() {
+  static const unsigned long long salt = []() {
+    std::random_device rd;
+    return ((unsigned long long)rd() << 32) ^
+           ((unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count() << 16);
+  }();
+  static std::atomic<unsigned long long> counter{1};
+  return (salt & 0xFFFFFFFF00000000ull) | (counter.fetch_add(1) & 0xFFFFFFFFull);
+}
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1719,9 +1778,17 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
 
   if (a.canon) {
     a.tpc = tiles_per_cta(p, hp.G);
-    const size_t need = (size_t)(grid / SS) * a.tpc * p.B_r * BN * 4;  // tiles indexed by (range, column tile)
+    const size_t tiles_bytes = (size_t)(grid / SS) * a.tpc * p.B_r * BN * 4;  // tiles indexed by (range, column tile)
+    const size_t need = tiles_bytes + (size_t)grid * 8;                      // + one flag per CTA
     if (!hp.ws || hp.ws_bytes < need) return fail(BPS_ERR_INVALID_ARG, "workspace too small for the tc plan");
     a.W = reinterpret_cast<float*>(hp.ws);
+    a.ss = SS;
+    if (a.ab & 256) {  // BPS_TC_AB & 256: per-CTA publication flags instead of the whole-grid wait
+      // (measured equal on LS/grad/smalln: the combine's cost is its own latency after the last
+      // range, not the wait for the grid — profiles/r02_narrow_n.md; kept as an experiment)
+      a.flags = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(hp.ws) + tiles_bytes);
+      a.epoch = next_epoch();
+    }
   }
 
   // TMA descriptor for the data operand

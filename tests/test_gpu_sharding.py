@@ -283,3 +283,20 @@ def test_block_sharded_apply_fused_nccl_world1():
             assert torch.equal(Y, ref), f"multicast={mc}"
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", [CASES[0], CASES[1], CASES[2], CASES[5]], ids=[IDS[0], IDS[1], IDS[2], IDS[5]])
+def test_combine_flag_handoff(case):
+    """The combine pass folds each straddling output once the CTAs holding its pieces have published
+    them (per-CTA epoch flags in the workspace, BPS_TC_AB=256, no whole-grid wait): bitwise equal to
+    the default whole-grid wait, over repeated calls on one workspace (stale flags of earlier launches)."""
+    layout, n, dt, mode = case
+    sk = Sketch(*layout, seed=39, mode=mode)
+    A = torch.randn((sk.d, n), device="cuda").to(_tdt(dt))
+    ref = sk.apply(A, variant="tc")
+    os.environ["BPS_TC_AB"] = "256"
+    try:
+        for _ in range(4):
+            assert torch.equal(sk.apply(A, variant="tc"), ref)
+    finally:
+        del os.environ["BPS_TC_AB"]
