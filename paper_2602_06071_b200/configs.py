@@ -53,6 +53,10 @@ LS = Config("ls", d=1 << 20, k=4096, kappa=4, s=4, n=512, dtype="f32", B_r=32)
 GRAD = Config("grad", d=1 << 24, k=8192, kappa=8, s=2, n=4096, dtype="bf16", B_r=16)
 # narrow inputs (per-example gradient batches, P:1841-1842 low-occupancy case): d large, n small
 SMALLN = Config("smalln", d=1 << 24, k=8192, kappa=8, s=2, n=32, dtype="bf16", B_r=16)
+# narrow-n experiments (profiles/r02_narrow_n.md): the smalln shape with fewer band entries per input row
+SMALLN_K4 = Config("smalln_k4", d=1 << 24, k=8192, kappa=4, s=2, n=32, dtype="bf16", B_r=16)
+SMALLN_K2 = Config("smalln_k2", d=1 << 24, k=8192, kappa=2, s=2, n=32, dtype="bf16", B_r=16)
+SMALLN_K1 = Config("smalln_k1", d=1 << 24, k=8192, kappa=1, s=1, n=32, dtype="bf16", B_r=16)
 SCALEOUT = Config("scaleout", d=1 << 26, k=16384, kappa=8, s=4, n=16384, dtype="bf16", B_r=16)
 
 
@@ -74,4 +78,4 @@ SWEEP_TUNED = [sweep_tuned(k, s, dt) for dt in ("bf16", "f32") for k in (1, 2, 4
 # 256 KiB per bf16 vector) and many of them, same bytes as the sweep
 TPROBE = Config("tprobe", d=1 << 17, k=4096, kappa=4, s=4, n=32768, dtype="bf16", B_r=32)
 TPROBE2 = Config("tprobe2", d=1 << 19, k=4096, kappa=4, s=4, n=8192, dtype="bf16", B_r=32)
-CONFIGS = {c.name: c for c in [TINY, LS, GRAD, SMALLN, SCALEOUT, TPROBE, TPROBE2] + SWEEP + SWEEP_TUNED}
+CONFIGS = {c.name: c for c in [TINY, LS, GRAD, SMALLN, SMALLN_K4, SMALLN_K2, SMALLN_K1, SCALEOUT, TPROBE, TPROBE2] + SWEEP + SWEEP_TUNED}
