@@ -70,6 +70,19 @@ struct Cfg {
   // CTA issues 1/SS of the rows).  Band sharing across column tiles (CS) is off then.
   static_assert(SS == 1 || (CS == 1 && NMT == 1 && !TRANS && !TF && !RL), "SS: row-major NT form, one band tile");
   static constexpr int CL = CS * SS;  // cluster size
+  // PAIR (bf16, SS = 2): the two CTAs run ONE cta_group::2 MMA of M = 256 — each holds its 128 band
+  // rows (A) and HALF of the data columns (B); D = its rows × all columns in its own TMEM.  The data
+  // tile is loaded once (each CTA its half) instead of multicast whole to both, halving the
+  // shared-memory write and read of the data per SM.  Only the leader (rank 0) issues MMAs.
+  // Built and parity-green (-DBPS_TC_PAIR=1, scripts/pair_smoke.py), but measured 2.0-2.1x SLOWER
+  // than the multicast slot split on the κ = 8 sweep (1.8 vs 3.7 TB/s), also with no MMA and no band
+  // generation — not the 2-CTA TMA form, the cluster-scope waits or the proxy fences (each swapped
+  // out, profiles/r02_narrow_n.md); off by default.
+#ifndef BPS_TC_PAIR
+#define BPS_TC_PAIR 0
+#endif
+  static constexpr bool PAIR = BPS_TC_PAIR && SS == 2 && !F32;
+  static constexpr int BNL = PAIR ? BN_ / 2 : BN_;  // data columns held in this CTA's shared memory
   // RL ("re-layout", bf16 transposed layout only): TMA loads TWO K-chunks per box without
   // swizzle (256-byte runs per vector: with vectors megabytes apart, 128-byte runs stream at
   // ~4.6 TB/s and 256-byte runs at ~7.2 TB/s, scripts/tma_probe.cu), into two consecutive ring
@@ -83,7 +96,7 @@ struct Cfg {
   static_assert(!TF || (F32 && !TRANS && NMT == 1 && BN_ == 128), "TF: fp32 row-major, one band tile");
   static constexpr int BN = BN_;  // data columns per CTA; TMEM = D (NMT·BN) + S (NMT·BN)
   static constexpr int ESZ = F32 ? 4 : 2;
-  static constexpr int RAW_STAGE = kBK * BN * ESZ;
+  static constexpr int RAW_STAGE = kBK * BNL * ESZ;
   static constexpr int CONV_HALF = kBK * BN * 2;  // fp32: hi and lo bf16 tiles overwrite the raw stage in place
   static constexpr int BAND_STAGE = NMT * kBandTile;
   // CS > 1: the CTAs of a cluster (same input range, CS column tiles) share the band — band
@@ -145,7 +158,7 @@ struct Cfg {
   static constexpr int OFF_D1 = OFF_TA + NCONVA * 64;       // TF: second D buffer
   static constexpr int TMEM_NEED = OFF_D1 + (TF ? DN : 0);
   static constexpr uint32_t TMEM_COLS = (TMEM_NEED <= 256) ? 256 : 512;
-  static constexpr uint32_t IDESC = ptx::idesc_bf16(128, DN, TF ? false : !TRANS);
+  static constexpr uint32_t IDESC = ptx::idesc_bf16(PAIR ? 256 : 128, DN, TF ? false : !TRANS);
   static_assert(NRAW >= 2, "smem: raw ring");
   static_assert(TMEM_NEED <= 512 && DN <= 256, "TMEM / MMA N");
   static_assert(BN % 64 == 0 && BN <= 256, "BN");
@@ -471,17 +484,20 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
   const int S0i = (int)S0, S1i = (int)S1, sbi = (int)sb;
   if (threadIdx.x == 0) {
     for (int i = 0; i < K::NRAW; ++i) {
-      ptx::mbar_init(&raw_full[i], 1);
-      ptx::mbar_init(&raw_empty[i], TF ? K::NCONVW * kArrivePerWarp : SS);  // TF: converter warps; SS: every CTA's MMA
+      // PAIR leader: its own TMA bytes + the peer's forwarded "my half landed" arrival
+      ptx::mbar_init(&raw_full[i], (K::PAIR && css == 0) ? 2 : 1);
+      // TF: converter warps; SS: every CTA's MMA (multicast data); PAIR: the leader's pair commit
+      ptx::mbar_init(&raw_empty[i], TF ? K::NCONVW * kArrivePerWarp : (K::PAIR ? 1 : SS));
       ptx::mbar_init(&conv_full[i], K::NCONVW > 0 ? K::NCONVW * kArrivePerWarp : 1);
     }
     for (int i = 0; i < K::NBAND; ++i) {
-      ptx::mbar_init(&band_full[i], CS > 1 ? 1 : K::NBW * kArrivePerWarp);
+      // PAIR: the leader's band warps and (one arrival per warp) the peer's
+      ptx::mbar_init(&band_full[i], CS > 1 ? 1 : K::NBW * kArrivePerWarp + (K::PAIR ? K::NBW : 0));
       ptx::mbar_init(&band_empty[i], CS);
     }
     for (int i = 0; i < K::NACC; ++i) {
       ptx::mbar_init(&acc_full[i], 1);
-      ptx::mbar_init(&acc_free[i], 128);
+      ptx::mbar_init(&acc_free[i], K::PAIR ? 256 : 128);  // PAIR: both CTAs' epilogues (leader's barrier)
     }
     for (int i = 0; i < K::NCONVA; ++i) {
       ptx::mbar_init(&ta_full[i], K::NCONVW > 0 ? K::NCONVW * kArrivePerWarp : 1);
@@ -492,7 +508,12 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
     ptx::tma_prefetch(&tmap);
   }
   if (threadIdx.x < 40) reinterpret_cast<uint32_t*>(smem + K::OFF_FIX)[threadIdx.x] = 0u;
-  if (warp == K::W_MMA) ptx::tmem_alloc(tmem_ptr, K::TMEM_COLS);
+  if (warp == K::W_MMA) {
+    if (K::PAIR)
+      ptx::tmem_alloc_pair(tmem_ptr, K::TMEM_COLS);
+    else
+      ptx::tmem_alloc(tmem_ptr, K::TMEM_COLS);
+  }
   ptx::tc_fence_before();
   if (K::CL > 1)
     ptx::cluster_sync();  // peers' barriers are initialised before any remote copy/arrive
@@ -588,10 +609,17 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
             } else {
               wait_slot(&raw_empty[s], ph ^ 1, args.sleep_ns);
               tr.add(0, t0);
-              ptx::mbar_arrive_expect_tx(&raw_full[s], K::RAW_STAGE);
+              if (!K::PAIR) ptx::mbar_arrive_expect_tx(&raw_full[s], K::RAW_STAGE);
               uint8_t* dst = smem + K::OFF_RAW + s * K::RAW_STAGE;
               const int32_t r = (int32_t)(row0 + kc * kBK);
-              if (SS > 1) {
+              if (K::PAIR) {
+                // CTA pair: this CTA loads its half of the columns into its own ring slot; the peer's
+                // MMA warp forwards the landing of its half to the leader's barrier
+                ptx::mbar_arrive_expect_tx(&raw_full[s], K::RAW_STAGE);
+#pragma unroll
+                for (int b = 0; b < K::BNL / 64; ++b)
+                  ptx::tma_load_2d(dst + b * (kBK * 128), &tmap, &raw_full[s], (int32_t)(col0 + css * K::BNL + 64 * b), r, pol);
+              } else if (SS > 1) {
                 // slot split: this CTA loads rows [css·PR, (css+1)·PR) of the stage and multicasts them
                 // to the SS CTAs of the cluster (same smem offset, completing tx on each one's raw_full)
                 constexpr int PR = kBK / SS;
@@ -623,7 +651,18 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         }
         tr.add(1, tstart);
       }
-    } else if (warp == K::W_MMA) {
+    } else if (K::PAIR && warp == K::W_MMA && css != 0) {
+      // ============ PAIR peer: forward "my half of stage s landed" to the leader's barrier ============
+      if (lane == 0) {
+        int s = 0;
+        uint32_t ph = 0;
+        for (int st = S0i; st < S1i; ++st) {
+          ptx::mbar_wait(&raw_full[s], ph);
+          ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&raw_full[s]), 0));
+          if (++s == K::NRAW) s = 0, ph ^= 1;
+        }
+      }
+    } else if (warp == K::W_MMA) {  // PAIR: the leader issues for both CTAs
       // ===================== MMA issuer =====================
       // The whole warp runs the loop (descriptors stay warp-uniform, in uniform registers);
       // one elected lane issues the tcgen05.mma / commit instructions.
@@ -658,7 +697,10 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               dbuf = gcount % K::NACC;
               if (gcount >= K::NACC) {  // this D buffer must have been folded into S
                 const unsigned long long t0 = tr.now();
-                ptx::mbar_wait(&acc_free[dbuf], (uint32_t)(gcount / K::NACC - 1) & 1u);
+                if (K::PAIR && (args.ab & 512))
+                  ptx::mbar_wait_cluster(&acc_free[dbuf], (uint32_t)(gcount / K::NACC - 1) & 1u);
+                else
+                  ptx::mbar_wait(&acc_free[dbuf], (uint32_t)(gcount / K::NACC - 1) & 1u);
                 tr.add(2, t0);
                 ptx::tc_fence_after();
               }
@@ -671,7 +713,14 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               // data stage and band stage of this step, polled together
               uint64_t* db = TF ? &ta_full[(st - S0i) & 1] : &dfull[(!TRANS && args.kgroup > 1) ? (ds & ~(args.kgroup - 1)) : ds];
               const uint32_t dp = TF ? ((uint32_t)((st - S0i) >> 1) & 1u) : dph;
-              ptx::mbar_wait2(db, dp, &band_full[bs], bph);
+              // (PAIR: the peer's band warps and data forwarder arrive here too, with cluster-scope
+              // release; a cluster-scope acquire poll measured ~2.5x slower than this wait)
+              if (K::PAIR && (args.ab & 512)) {
+                while (!ptx::mbar_try_wait2_cluster(db, dp, &band_full[bs], bph)) {
+                }
+              } else {
+                ptx::mbar_wait2(db, dp, &band_full[bs], bph);
+              }
             }
             tr.add(3, t0);
             ptx::tc_fence_after();
@@ -698,7 +747,12 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
                 // data: K-major (+32 B per K-step) or MN-major (+16 rows of 128 B per K-step)
                 const uint64_t bdesc = b0hi | (blo + (uint32_t)(TRANS ? ks * 2 : ks * 128));
                 const uint32_t acc = (gstart && ks == 0) ? 0u : 1u;  // fresh per group
-                if (!BPS_DBG(4)) ptx::mma_bf16_ss(tmem + m * K::DN, adesc, bdesc, K::IDESC, acc);
+                if (BPS_DBG(4)) {
+                } else if (K::PAIR) {
+                  ptx::mma_bf16_ss_pair(tmem + m * K::DN, adesc, bdesc, K::IDESC, acc);
+                } else {
+                  ptx::mma_bf16_ss(tmem + m * K::DN, adesc, bdesc, K::IDESC, acc);
+                }
               }
             }
             if (BPS_DBG(64)) {  // experiment (with dbg 4, no MMA issued): release by a thread arrive
@@ -706,17 +760,26 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               ptx::mbar_arrive(&band_empty[bs]);
             } else if (TF)
               ptx::mma_commit(&ta_empty[(st - S0i) & 1]);
+            else if (K::PAIR)
+              ptx::mma_commit_pair(&dempty[ds], (uint16_t)3u);  // both CTAs' halves were read
             else if (SS > 1)
               ptx::mma_commit_multicast(&dempty[ds], (uint16_t)((1u << SS) - 1u));  // every CTA's copy was filled
             else
               ptx::mma_commit(&dempty[ds]);
             if (BPS_DBG(64) || sp != ksm)
               ;  // kstep = 2: the pair's buffers are released together, on its first buffer
+            else if (K::PAIR)
+              ptx::mma_commit_pair(&band_empty[bs], (uint16_t)3u);  // both CTAs' band stages
             else if (CS > 1)
               ptx::mma_commit_multicast(&band_empty[bs], (uint16_t)((1u << CS) - 1));
             else
               ptx::mma_commit(&band_empty[bs - ksm]);
-            if (gend) ptx::mma_commit(&acc_full[dbuf]);
+            if (gend) {
+              if (K::PAIR)
+                ptx::mma_commit_pair(&acc_full[dbuf], (uint16_t)3u);  // D is ready in both TMEMs
+              else
+                ptx::mma_commit(&acc_full[dbuf]);
+            }
             }  // elect_one
             __syncwarp();
             if (gend) ++gcount;
@@ -965,7 +1028,10 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&acc_free[db]);
+        if (K::PAIR && css != 0)
+          ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&acc_free[db]), 0));  // the leader's MMA waits
+        else
+          ptx::mbar_arrive(&acc_free[db]);
         // ---- group-end bookkeeping (uniform over the 128 epilogue threads)
         if (blk_end && mine(q - kap) && role(q - kap) == 1 && bar_red_or(kEpiBar, 128, mybad)) fix_output(q - kap);
       }
@@ -1295,6 +1361,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               if (++bs == K::NBAND) bs = 0, bph ^= 1;
               continue;
             }
+            // (PAIR: this CTA's band rows are read by its own SM's tensor core, as part of the leader's
+            // pair MMA — the CTA-scope proxy fence plus the cluster-release arrive order them)
             if (!BPS_DBG(16)) ptx::fence_proxy_async_smem();
             if (CS > 1) {
               ptx::named_bar_sync(3, K::NBANDT);  // whole stage written (and fenced) by all band threads
@@ -1308,7 +1376,12 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
                 ptx::mbar_arrive(&band_full[bs]);
               }
             } else {
-              warp_arrive(&band_full[bs - ksm]);
+              if (K::PAIR && css != 0) {  // the leader's MMA reads this CTA's band rows
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&band_full[bs]), 0));
+              } else {
+                warp_arrive(&band_full[bs - ksm]);
+              }
             }
             if (++bs == K::NBAND) bs = 0, bph ^= 1;
           }
@@ -1480,7 +1553,10 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
   tr_cta.add(15, t_cta0);
   if (warp == K::W_MMA) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, K::TMEM_COLS);
+    if (K::PAIR)
+      ptx::tmem_dealloc_pair(tmem, K::TMEM_COLS);
+    else
+      ptx::tmem_dealloc(tmem, K::TMEM_COLS);
   }
   // this CTA's stores are issued: let the combine kernel (programmatic dependent launch) start its
   // prologue; it reads our data only after griddepcontrol.wait (full completion of this grid)
@@ -1802,7 +1878,7 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     dims[0] = (cuuint64_t)n;
     dims[1] = (cuuint64_t)in_rows;
     box[0] = F32 ? BN : 64;
-    box[1] = SS > 1 ? kBK / SS : kBK * a.kgroup;  // SS: each CTA of the cluster loads 1/SS of the rows
+    box[1] = (SS > 1 && !K::PAIR) ? kBK / SS : kBK * a.kgroup;  // SS: each CTA of the cluster loads 1/SS of the rows
   } else {
     dims[0] = (cuuint64_t)in_rows;  // coordinates (d)
     dims[1] = (cuuint64_t)n;        // vectors
