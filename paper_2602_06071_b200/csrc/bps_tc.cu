@@ -120,11 +120,16 @@ Choice choose(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, c
   c.trans = transposed;
   c.nmt = nmt;
   c.ss = ss;
-  if (ss > 1) {  // slot split: one band tile per CTA, NT form, no band sharing across column tiles
-    c.tf = c.rl = false;
+  if (ss > 1) {  // slot split: one band tile per CTA, no band sharing across column tiles
+    c.rl = false;
     c.cs = 1;
     if (c.f32) {
       c.bn = 128;
+      // fp32: NT form (hi/lo split in shared memory).  BPS_TC_FORM=tf: the T form (each CTA converts
+      // the multicast stage into its TMEM A operand, the ring slot released by every CTA's converters)
+      // — parity-green, measured 1.4-2.2x slower on the κ = 8 / 16 fp32 sweep points
+      const char* fe = getenv("BPS_TC_FORM");
+      c.tf = !transposed && fe && std::string(fe) == "tf";
     } else {
       const int64_t ct256 = (n + 255) / 256, ct128 = (n + 127) / 128, cl = std::max(1, sms / ss);
       const int64_t used256 = ct256 >= cl ? ct256 : ct256 * (cl / ct256);

@@ -59,7 +59,9 @@ struct HostPlan {
   X(false, false, 1, 128, 1, false, false, 2)                                                     \
   X(false, false, 1, 128, 1, false, false, 4)                                                     \
   X(true, false, 1, 128, 1, false, false, 2)                                                      \
-  X(true, false, 1, 128, 1, false, false, 4)
+  X(true, false, 1, 128, 1, false, false, 4)                                                      \
+  X(true, false, 1, 128, 1, true, false, 2)   /* fp32 slot split in the T form (data in TMEM)    */ \
+  X(true, false, 1, 128, 1, true, false, 4)
 
 template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL, int SS>
 int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, float* Y, int64_t ldy,

@@ -54,6 +54,9 @@ namespace bps {
 namespace tcx {
 namespace {
 
+#ifndef BPS_WARP_ARRIVE
+#define BPS_WARP_ARRIVE 1
+#endif
 constexpr int kBandTile = 128 * kBK * 2;  // one M-tile (128 band rows) of a band stage, bytes
 constexpr int kMaxRanges = 511;           // canon: stream ranges per column tile (TcArgs::rb)
 constexpr int kMaxPeers = 8;              // output broadcast destinations (TcArgs::peer)
@@ -68,7 +71,10 @@ struct Cfg {
   // take the same range and column tile and split the κ band slots — κ/SS slots (≤ 128 band rows,
   // one M-tile) each; the data stage is loaded once from HBM and multicast to all of them (each
   // CTA issues 1/SS of the rows).  Band sharing across column tiles (CS) is off then.
-  static_assert(SS == 1 || (CS == 1 && NMT == 1 && !TRANS && !TF && !RL), "SS: row-major NT form, one band tile");
+  static_assert(SS == 1 || (CS == 1 && NMT == 1 && !TRANS && !RL), "SS: row-major, one band tile");
+  // TF with SS (fp32): every CTA converts the multicast stage into its own TMEM A operand; a ring
+  // slot is free once the converters of ALL the cluster's CTAs have read it (one arrival per warp)
+  static_assert(!(TF && SS > 1) || BPS_WARP_ARRIVE, "TF slot split counts warp arrivals");
   static constexpr int CL = CS * SS;  // cluster size
   // PAIR (bf16, SS = 2): the two CTAs run ONE cta_group::2 MMA of M = 256 — each holds its 128 band
   // rows (A) and HALF of the data columns (B); D = its rows × all columns in its own TMEM.  The data
@@ -348,9 +354,6 @@ __device__ __forceinline__ float ld_cg_f(const float* p) {
 // shared-memory / TMEM accesses are ordered before lane 0's release-arrive by __syncwarp, so the
 // barrier sees one arrival per warp instead of 32 (per-thread arrivals on one barrier serialise
 // in the barrier unit; 256 of them per stage bounded the narrow-tile pipeline).
-#ifndef BPS_WARP_ARRIVE
-#define BPS_WARP_ARRIVE 1
-#endif
 constexpr int kArrivePerWarp = BPS_WARP_ARRIVE ? 1 : 32;
 __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
 #if BPS_WARP_ARRIVE
@@ -487,7 +490,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
       // PAIR leader: its own TMA bytes + the peer's forwarded "my half landed" arrival
       ptx::mbar_init(&raw_full[i], (K::PAIR && css == 0) ? 2 : 1);
       // TF: converter warps; SS: every CTA's MMA (multicast data); PAIR: the leader's pair commit
-      ptx::mbar_init(&raw_empty[i], TF ? K::NCONVW * kArrivePerWarp : (K::PAIR ? 1 : SS));
+      ptx::mbar_init(&raw_empty[i], TF ? SS * K::NCONVW * kArrivePerWarp : (K::PAIR ? 1 : SS));
       ptx::mbar_init(&conv_full[i], K::NCONVW > 0 ? K::NCONVW * kArrivePerWarp : 1);
     }
     for (int i = 0; i < K::NBAND; ++i) {
@@ -1424,6 +1427,11 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
 #pragma unroll
         for (int r = 0; r < 32; ++r) a[r] = raw[r * BN];
         warp_arrive(&raw_empty[rs]);  // values are in registers
+        if (SS > 1) {  // the multicast refill writes every CTA's copy: release the slot in all of them
+          if (lane == 0)
+            for (uint32_t pr = 1; pr < (uint32_t)SS; ++pr)
+              ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&raw_empty[rs]), ((uint32_t)css + pr) % SS));
+        }
         if (++rs == K::NRAW) rs = 0, rph ^= 1;
         const uint32_t ab = (uint32_t)(it & 1);
         ptx::mbar_wait(&ta_empty[ab], (uint32_t)((it >> 1) & 1) ^ 1u);
