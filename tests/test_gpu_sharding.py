@@ -300,3 +300,23 @@ def test_combine_flag_handoff(case):
             assert torch.equal(sk.apply(A, variant="tc"), ref)
     finally:
         del os.environ["BPS_TC_AB"]
+
+
+@pytest.mark.parametrize("layout", [(32, 32, 2048, 16, 4), (32, 32, 2048, 8, 4), (64, 16, 1024, 16, 2)])
+def test_fp32_slot_split_t_form(layout):
+    """fp32 κ·B_r in (128, 512] in the optional T form (BPS_TC_FORM=tf: the slot-split cluster's CTAs
+    convert the multicast stage into TMEM) — within the fp32 criterion of the oracle (the T form folds
+    the hi and lo products in one accumulator, the NT form adds them after: not bitwise equal)."""
+    sk = Sketch(*layout, seed=40)
+    osk = oracle.make_sketch(*layout, 40)
+    A = synth.host_matrix("gaussian", sk.d, 200, seed=2)
+    At = torch.from_numpy(A).cuda()
+    ref = sk.apply(At, variant="tc")
+    os.environ["BPS_TC_FORM"] = "tf"
+    try:
+        Y = sk.apply(At, variant="tc")
+    finally:
+        del os.environ["BPS_TC_FORM"]
+    torch.cuda.synchronize()
+    assert_f32(Y.cpu().numpy(), oracle.apply(osk, A), np.linalg.norm(A.astype(np.float64), axis=0), str(layout))
+    assert_f32(ref.cpu().numpy(), oracle.apply(osk, A), np.linalg.norm(A.astype(np.float64), axis=0), str(layout))
