@@ -151,8 +151,10 @@ Choice choose(const SketchParams& p, int64_t n, bps_dtype dt, bool transposed, c
     const int64_t used128 = ct128 >= sms ? ct128 : ct128 * (sms / ct128);
     c.bn = (used256 * 10 >= used128 * 9 || used256 >= sms) ? 256 : 128;
     if (n <= 64 && !transposed) c.bn = 64;
+    // n ≤ 32: a 32-column SW64 tile (no zero-filled half box, half the B-operand reads); BPS_TC_BN=64 off
+    if (n <= 32 && !transposed) c.bn = 32;
     if (const char* e = getenv("BPS_TC_BN"))  // tuning knob
-      c.bn = atoi(e) == 128 ? 128 : (atoi(e) == 64 && !transposed ? 64 : 256);
+      c.bn = atoi(e) == 128 ? 128 : (atoi(e) == 64 && !transposed ? 64 : (atoi(e) == 32 && !transposed && n <= 32 ? 32 : 256));
   } else {
     c.bn = nmt == 2 ? 128 : 64;
   }

@@ -37,6 +37,7 @@ struct HostPlan {
   X(false, false, 1, 128, 1, false, false, 1)                                                        \
   X(false, false, 1, 128, 2, false, false, 1)                                                        \
   X(false, false, 1, 64, 1, false, false, 1)  /* narrow n                                          */ \
+  X(false, false, 1, 32, 1, false, false, 1)  /* n <= 32: one SW64 atom                            */ \
   X(false, false, 1, 64, 2, false, false, 1)                                                         \
   X(false, true, 1, 256, 1, false, true, 1)   /* bf16 transposed: K-pair boxes + re-layout         */ \
   X(false, true, 1, 256, 2, false, true, 1)                                                          \

@@ -6,3 +6,4 @@ BPS_TC_DEFINE(true, false, 2, 64, 2, false, false, 1)
 BPS_TC_DEFINE(false, false, 1, 64, 2, false, false, 1)
 BPS_TC_DEFINE(false, true, 1, 128, 2, false, false, 1)
 BPS_TC_DEFINE(false, true, 4, 64, 2, false, false, 1)
+BPS_TC_DEFINE(false, false, 1, 32, 1, false, false, 1)

@@ -121,7 +121,7 @@ struct Cfg {
   static constexpr int NRAW_FIT = (BUDGET - NBAND * BAND_STAGE) / RAW_STAGE;
   // ring depth: 8 stages, 16 for the narrow tile (BN = 64, small n: 8 KB stages, so that enough
   // bytes are in flight)
-  static constexpr int NRAW_MAX = BN_ <= 64 && !F32 ? 16 : 8;
+  static constexpr int NRAW_MAX = BN_ <= 32 && !F32 ? 24 : (BN_ <= 64 && !F32 ? 16 : 8);
   static constexpr int NRAW = (NRAW_FIT > NRAW_MAX ? NRAW_MAX : NRAW_FIT) & (RL ? ~1 : ~0);  // RL: slot pairs
   static constexpr int OFF_RAW = 0;
   static constexpr int OFF_BAND = OFF_RAW + NRAW * RAW_STAGE;
@@ -167,7 +167,10 @@ struct Cfg {
   static constexpr uint32_t IDESC = ptx::idesc_bf16(PAIR ? 256 : 128, DN, TF ? false : !TRANS);
   static_assert(NRAW >= 2, "smem: raw ring");
   static_assert(TMEM_NEED <= 512 && DN <= 256, "TMEM / MMA N");
-  static_assert(BN % 64 == 0 && BN <= 256, "BN");
+  // BN = 32 (bf16 row-major, n ≤ 32): the data tile is one 64-byte-swizzled MN atom (32 columns ×
+  // 64 rows, TMA SWIZZLE_64B) — no zero-filled half as with a 64-column box
+  static_assert((BN % 64 == 0 || (BN == 32 && !F32 && !TRANS && !TF && SS == 1)) && BN <= 256, "BN");
+  static constexpr bool SW64 = BN == 32;
   static_assert(SMEM <= 227 * 1024, "smem");
 };
 
@@ -641,7 +644,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
                   ptx::tma_load_2d(dst, &tmap, &raw_full[s], (int32_t)col0, r, pol);
                 } else {
 #pragma unroll
-                  for (int b = 0; b < BN / 64; ++b)
+                  for (int b = 0; b < (BN + 63) / 64; ++b)
                     ptx::tma_load_2d(dst + b * (kBK * 128), &tmap, &raw_full[s], (int32_t)(col0 + 64 * b), r, pol);
                 }
               } else {
@@ -685,7 +688,11 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         // them per MMA was a ~45-instruction dependent uniform-datapath chain per stage that bounded
         // the narrow-tile pipeline (~650 cycles of issue per 64-row stage, ncu source view).
         const uint64_t a0 = ptx::smem_desc_sw128(band_base, 0, 1024);  // band, K-major
-        const uint64_t b0 = TRANS ? ptx::smem_desc_sw128(data_base, 0, 1024) : ptx::smem_desc_sw128(data_base, kBK * 128, 1024);
+        // data: K-major SW128 (transposed), MN-major SW128 (64-column atoms, 8 KB apart), or MN-major
+        // SW64 (BN = 32: one 32-column atom, 8-row groups 512 B apart; layout type 4)
+        const uint64_t b0 = TRANS ? ptx::smem_desc_sw128(data_base, 0, 1024)
+                                  : (K::SW64 ? ((ptx::smem_desc_sw128(data_base, kBK * 64, 512) & ~(7ull << 61)) | (4ull << 61))
+                                             : ptx::smem_desc_sw128(data_base, kBK * 128, 1024));
         const uint32_t a0lo = (uint32_t)a0, b0lo = (uint32_t)b0;
         const uint64_t a0hi = a0 & 0xFFFFFFFF00000000ull, b0hi = b0 & 0xFFFFFFFF00000000ull;
         int gcount = 0, dbuf = 0;  // groups started; D buffer of the current group
@@ -748,7 +755,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               for (int m = 0; m < NMT; ++m) {
                 const uint64_t adesc = a0hi | (alo + (uint32_t)(m * (kBandTile >> 4) + ks * 2));
                 // data: K-major (+32 B per K-step) or MN-major (+16 rows of 128 B per K-step)
-                const uint64_t bdesc = b0hi | (blo + (uint32_t)(TRANS ? ks * 2 : ks * 128));
+                const uint64_t bdesc = b0hi | (blo + (uint32_t)(TRANS ? ks * 2 : (K::SW64 ? ks * 64 : ks * 128)));
                 const uint32_t acc = (gstart && ks == 0) ? 0u : 1u;  // fresh per group
                 if (BPS_DBG(4)) {
                 } else if (K::PAIR) {
@@ -1880,12 +1887,13 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
   const CUtensorMapDataType tdt = F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   cuuint64_t dims[2], strides[1];
   cuuint32_t box[2], estr[2] = {1, 1};
-  const CUtensorMapSwizzle swz = (F32 || RL) ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B;
+  const CUtensorMapSwizzle swz = (F32 || RL) ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                             : (K::SW64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
   strides[0] = (cuuint64_t)lda * K::ESZ;
   if (!TRANS) {
     dims[0] = (cuuint64_t)n;
     dims[1] = (cuuint64_t)in_rows;
-    box[0] = F32 ? BN : 64;
+    box[0] = F32 ? BN : (BN < 64 ? BN : 64);
     box[1] = (SS > 1 && !K::PAIR) ? kBK / SS : kBK * a.kgroup;  // SS: each CTA of the cluster loads 1/SS of the rows
   } else {
     dims[0] = (cuuint64_t)in_rows;  // coordinates (d)

@@ -320,3 +320,17 @@ def test_fp32_slot_split_t_form(layout):
     torch.cuda.synchronize()
     assert_f32(Y.cpu().numpy(), oracle.apply(osk, A), np.linalg.norm(A.astype(np.float64), axis=0), str(layout))
     assert_f32(ref.cpu().numpy(), oracle.apply(osk, A), np.linalg.norm(A.astype(np.float64), axis=0), str(layout))
+
+
+@pytest.mark.parametrize("case", [CASES[1], CASES[3], CASES[7]], ids=[IDS[1], IDS[3], IDS[7]])
+def test_narrow_tile_columns_bitwise(case):
+    """Column slices of ≤ 32 columns take the 32-column SW64 tile (bf16): bitwise equal to the same
+    columns of the wide-tile apply (the canonical fold does not depend on the tile width), and within
+    the oracle criterion."""
+    layout, n, dt, mode = case
+    sk = Sketch(*layout, seed=41, mode=mode)
+    A = torch.randn((sk.d, n), device="cuda").to(_tdt(dt))
+    Y = sk.apply(A, variant="tc")
+    for c0, w in [(0, 32), (8, 24), (n - 8, 8), (32, 16)]:  # widths: 16-byte aligned rows
+        Yn = sk.apply(A[:, c0:c0 + w].contiguous(), variant="tc")
+        assert torch.equal(Yn, Y[:, c0:c0 + w]), (c0, w)
