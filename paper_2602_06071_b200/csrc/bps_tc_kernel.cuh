@@ -117,11 +117,18 @@ struct Cfg {
   static constexpr int NBAND = CS > 1 ? (NBAND_CL < CS ? CS : NBAND_CL)
                                       : ((NMT == 1 && !F32) ? (BN_ <= 64 ? BPS_NBAND_NARROW : 3) : 2);
   static constexpr int LOCALB = NBAND / CS;  // band buffers this CTA generates into
-  static constexpr int BUDGET = 210 * 1024;
+  // MINB: CTAs per SM.  The 32-column narrow tile runs TWO CTAs per SM (≤ 72 registers, ≈ 104 KB
+  // of shared memory each): its per-stage cost is pipeline latency, not a saturated unit
+  // (profiles/r02_narrow_n.md), so a second independent pipeline per SM overlaps it
+#ifndef BPS_NARROW_MINB
+#define BPS_NARROW_MINB 2
+#endif
+  static constexpr int MINB = (BN_ <= 64 && NMT == 1 && !F32 && !TRANS && CS == 1 && SS == 1) ? BPS_NARROW_MINB : 1;
+  static constexpr int BUDGET = MINB == 2 ? 100 * 1024 : 210 * 1024;
   static constexpr int NRAW_FIT = (BUDGET - NBAND * BAND_STAGE) / RAW_STAGE;
   // ring depth: 8 stages, 16 for the narrow tile (BN = 64, small n: 8 KB stages, so that enough
   // bytes are in flight)
-  static constexpr int NRAW_MAX = BN_ <= 32 && !F32 ? 24 : (BN_ <= 64 && !F32 ? 16 : 8);
+  static constexpr int NRAW_MAX = BN_ <= 32 && !F32 ? (MINB == 2 ? 12 : 24) : (BN_ <= 64 && !F32 ? (MINB == 2 ? 8 : 16) : 8);
   static constexpr int NRAW = (NRAW_FIT > NRAW_MAX ? NRAW_MAX : NRAW_FIT) & (RL ? ~1 : ~0);  // RL: slot pairs
   static constexpr int OFF_RAW = 0;
   static constexpr int OFF_BAND = OFF_RAW + NRAW * RAW_STAGE;
@@ -433,7 +440,8 @@ __device__ float exact_elem(const TcArgs& a, int64_t i, uint32_t r, int64_t t, i
 }
 
 template <bool F32, bool TRANS, int NMT, int BN_, int CS, bool TF, bool RL, int SS>
-__global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTHREADS, 1)
+__global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTHREADS,
+                                  Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::MINB)
     bps_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TcArgs args) {
   using K = Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>;
   constexpr int BN = K::BN;
@@ -1806,9 +1814,11 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
   const int64_t n_ct = (n + BN - 1) / BN;
   int dev = 0;
   cudaGetDevice(&dev);
-  int slots = hp.sms;
+  int slots = hp.sms * K::MINB;
   auto kern = bps_tc_kernel<F32, TRANS, NMT, BN_, CS, TF, RL, SS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+  if (e == cudaSuccess && K::MINB > 1)  // room for MINB CTAs per SM
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return fail(BPS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
   if (K::CL > 1) {  // clusters must fit inside a GPC: not every SM can host one
     static std::atomic<int> cached_slots[64];
