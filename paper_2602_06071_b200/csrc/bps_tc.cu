@@ -192,7 +192,7 @@ size_t workspace_impl(const SketchParams& p, int64_t n, bps_dtype dt, bool trans
   const Choice c = choose(p, n, dt, transposed, pl, cv.nmt, cv.ss, sms, true, G);
   const int64_t nct = (n + c.bn - 1) / c.bn;
   // grid = nct·R ≤ max(nct, co-resident slots); the 32-column narrow tile runs 2 CTAs per SM (Cfg::MINB)
-  const int minb = (c.bn <= 64 && c.nmt == 1 && !c.f32 && !c.trans && c.cs == 1 && c.ss == 1) ? 2 : 1;
+  const int minb = narrow_minb(c.f32, c.trans, c.nmt, c.bn, c.cs, c.ss);
   const int64_t ctas = std::max<int64_t>(nct, (int64_t)sms * minb);
   // partial tiles + one 8-byte publication flag per CTA (slot-split clusters: ss CTAs per tile)
   return (size_t)ctas * (size_t)tiles_per_cta(p, G) * p.B_r * c.bn * 4 + (size_t)ctas * c.ss * 8;

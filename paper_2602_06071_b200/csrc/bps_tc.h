@@ -11,6 +11,21 @@ namespace tcx {
 
 constexpr int kBK = 64;  // K rows (input rows u) per pipeline stage
 
+// CTAs per SM of a kernel configuration: the narrow bf16 row-major tiles (one band tile, no cluster)
+// run several independent pipelines per SM — their per-stage cost is handshake latency
+// (profiles/r02_narrow_n.md): 2 for the 32- and 64-column tiles (3 for the 32-column tile with 4
+// band warps and 2 band buffers measured slower: 1146 vs 1388 GB/s); everything else one CTA per SM.
+#ifndef BPS_NARROW_MINB32
+#define BPS_NARROW_MINB32 2
+#endif
+#ifndef BPS_NARROW_MINB
+#define BPS_NARROW_MINB 2
+#endif
+constexpr int narrow_minb(bool f32, bool trans, int nmt, int bn, int cs, int ss) {
+  return (!f32 && !trans && nmt == 1 && cs == 1 && ss == 1) ? (bn == 32 ? BPS_NARROW_MINB32 : (bn == 64 ? BPS_NARROW_MINB : 1))
+                                                             : 1;
+}
+
 // Everything the host decided before choosing a template instantiation.
 struct HostPlan {
   int G;            // K-chunks per accumulation group: a function of the sketch only (canonical sums)

@@ -114,21 +114,16 @@ struct Cfg {
 #ifndef BPS_NBAND_NARROW
 #define BPS_NBAND_NARROW 3
 #endif
+  static constexpr int MINB = narrow_minb(F32, TRANS, NMT, BN_, CS, SS);  // CTAs per SM (bps_tc.h)
   static constexpr int NBAND = CS > 1 ? (NBAND_CL < CS ? CS : NBAND_CL)
-                                      : ((NMT == 1 && !F32) ? (BN_ <= 64 ? BPS_NBAND_NARROW : 3) : 2);
+                                      : ((NMT == 1 && !F32) ? (MINB >= 3 ? 2 : (BN_ <= 64 ? BPS_NBAND_NARROW : 3)) : 2);
   static constexpr int LOCALB = NBAND / CS;  // band buffers this CTA generates into
-  // MINB: CTAs per SM.  The 32-column narrow tile runs TWO CTAs per SM (≤ 72 registers, ≈ 104 KB
-  // of shared memory each): its per-stage cost is pipeline latency, not a saturated unit
-  // (profiles/r02_narrow_n.md), so a second independent pipeline per SM overlaps it
-#ifndef BPS_NARROW_MINB
-#define BPS_NARROW_MINB 2
-#endif
-  static constexpr int MINB = (BN_ <= 64 && NMT == 1 && !F32 && !TRANS && CS == 1 && SS == 1) ? BPS_NARROW_MINB : 1;
-  static constexpr int BUDGET = MINB == 2 ? 100 * 1024 : 210 * 1024;
+  static constexpr int BUDGET = MINB >= 3 ? 68 * 1024 : (MINB == 2 ? 100 * 1024 : 210 * 1024);
   static constexpr int NRAW_FIT = (BUDGET - NBAND * BAND_STAGE) / RAW_STAGE;
   // ring depth: 8 stages, 16 for the narrow tile (BN = 64, small n: 8 KB stages, so that enough
   // bytes are in flight)
-  static constexpr int NRAW_MAX = BN_ <= 32 && !F32 ? (MINB == 2 ? 12 : 24) : (BN_ <= 64 && !F32 ? (MINB == 2 ? 8 : 16) : 8);
+  static constexpr int NRAW_MAX = BN_ <= 32 && !F32 ? (MINB >= 3 ? 8 : (MINB == 2 ? 12 : 24))
+                                                   : (BN_ <= 64 && !F32 ? (MINB == 2 ? 8 : 16) : 8);
   static constexpr int NRAW = (NRAW_FIT > NRAW_MAX ? NRAW_MAX : NRAW_FIT) & (RL ? ~1 : ~0);  // RL: slot pairs
   static constexpr int OFF_RAW = 0;
   static constexpr int OFF_BAND = OFF_RAW + NRAW * RAW_STAGE;
@@ -153,7 +148,7 @@ struct Cfg {
 #ifndef BPS_NBW
 #define BPS_NBW 8
 #endif
-  static constexpr int NBW = BPS_NBW;  // band generator warps (4 .. 4+NBW-1)
+  static constexpr int NBW = MINB >= 3 ? 4 : BPS_NBW;  // band generator warps (4 .. 4+NBW-1)
   static_assert(NBW % 4 == 0 && NBW >= 4 && NBW <= 16, "band warps");
   static constexpr int W_CONV0 = 4 + NBW;  // fp32 converter warps W_CONV0 .. W_CONV0+7
   static constexpr int NCONVW = F32 ? 8 : (RL ? BN_ / 32 : 0);  // converter (fp32 split / RL re-layout) warps
