@@ -199,6 +199,7 @@ struct TcArgs {
   int G;                       // K-chunks per accumulation group (divides B_c/64; sketch-only)
   int kgroup;                  // transposed layout: K-chunks whose TMA loads are issued together (≤ NRAW)
   int kstep;                   // stages per band/MMA handshake (1 or 2; 2: narrow bf16 tile, see bps_tc_kernel)
+  int band_mn;                 // 1: MN-major band tile written as 16-byte one-hot pieces (C = 8, B_r % 8 == 0)
   int tbox;                    // transposed layout, kgroup > 1: vectors per TMA box (divides BN)
   int nohoist;                 // A/B knob: 1 disables the band generator's register-resident keys
   uint32_t mma_hint;           // MMA issuer's mbarrier suspend-time hint (ns)
@@ -690,7 +691,11 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         // addresses < 228 KB never carry out of it) moves by the ring slot and the K-step.  Rebuilding
         // them per MMA was a ~45-instruction dependent uniform-datapath chain per stage that bounded
         // the narrow-tile pipeline (~650 cycles of issue per 64-row stage, ncu source view).
-        const uint64_t a0 = ptx::smem_desc_sw128(band_base, 0, 1024);  // band, K-major
+        // band: K-major (+32 B per K-step), or MN-major (band_mn: 64-row atoms 8 KB apart, +16 rows of
+        // 128 B per K-step) with the matching major bit in the instruction descriptor
+        const uint64_t a0 = args.band_mn ? ptx::smem_desc_sw128(band_base, kBK * 128, 1024) : ptx::smem_desc_sw128(band_base, 0, 1024);
+        const uint32_t band_ks = args.band_mn ? 128u : 2u;
+        const uint32_t idesc = K::IDESC | (args.band_mn ? (TF ? (1u << 16) : (1u << 15)) : 0u);
         // data: K-major SW128 (transposed), MN-major SW128 (64-column atoms, 8 KB apart), or MN-major
         // SW64 (BN = 32: one 32-column atom, 8-row groups 512 B apart; layout type 4)
         const uint64_t b0 = TRANS ? ptx::smem_desc_sw128(data_base, 0, 1024)
@@ -744,11 +749,11 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               const uint32_t ta = tmem_A + (uint32_t)((st - S0i) & 1) * 64;
 #pragma unroll
               for (int ks = 0; ks < kBK / 16; ++ks) {
-                const uint64_t bdesc = a0hi | (alo + ks * 2);  // band, K-major: +32 B per K-step
+                const uint64_t bdesc = a0hi | (alo + ks * band_ks);  // band (B operand of the T form)
                 if (!BPS_DBG(4)) {
                   const uint32_t dt = tmem + (dbuf ? K::OFF_D1 : 0);
-                  ptx::mma_bf16_ts(dt, ta + ks * 8, bdesc, K::IDESC, (gstart && ks == 0) ? 0u : 1u);  // hi
-                  ptx::mma_bf16_ts(dt, ta + 32 + ks * 8, bdesc, K::IDESC, 1u);                          // lo
+                  ptx::mma_bf16_ts(dt, ta + ks * 8, bdesc, idesc, (gstart && ks == 0) ? 0u : 1u);  // hi
+                  ptx::mma_bf16_ts(dt, ta + 32 + ks * 8, bdesc, idesc, 1u);                          // lo
                 }
               }
             } else
@@ -756,15 +761,15 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
             for (int ks = 0; ks < kBK / 16; ++ks) {
 #pragma unroll
               for (int m = 0; m < NMT; ++m) {
-                const uint64_t adesc = a0hi | (alo + (uint32_t)(m * (kBandTile >> 4) + ks * 2));
+                const uint64_t adesc = a0hi | (alo + (uint32_t)(m * (kBandTile >> 4)) + (uint32_t)ks * band_ks);
                 // data: K-major (+32 B per K-step) or MN-major (+16 rows of 128 B per K-step)
                 const uint64_t bdesc = b0hi | (blo + (uint32_t)(TRANS ? ks * 2 : (K::SW64 ? ks * 64 : ks * 128)));
                 const uint32_t acc = (gstart && ks == 0) ? 0u : 1u;  // fresh per group
                 if (BPS_DBG(4)) {
                 } else if (K::PAIR) {
-                  ptx::mma_bf16_ss_pair(tmem + m * K::DN, adesc, bdesc, K::IDESC, acc);
+                  ptx::mma_bf16_ss_pair(tmem + m * K::DN, adesc, bdesc, idesc, acc);
                 } else {
-                  ptx::mma_bf16_ss(tmem + m * K::DN, adesc, bdesc, K::IDESC, acc);
+                  ptx::mma_bf16_ss(tmem + m * K::DN, adesc, bdesc, idesc, acc);
                 }
               }
             }
@@ -1120,8 +1125,11 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         // offsets), the row offset is a shift, and the stale entries are kept as 16-bit entry
         // offsets (clearing = one extract + one store).  C = 1 (s = B_r) writes every band row of
         // every column each stage, so nothing needs clearing at all.
-        constexpr bool FAST = decltype(fast_tag)::value >= 1;
-        constexpr bool FULL = decltype(fast_tag)::value >= 2;  // κs a multiple of 4·NCG: no batch tail
+        // MN8 (C = 8, B_r % 8 == 0, TcArgs::band_mn): MN-major band tile — a chunk's 8 rows at input
+        // row u are one 16-byte piece, written whole (one-hot) each stage: no clearing, no prev state
+        constexpr bool MN8 = decltype(fast_tag)::value == 7;
+        constexpr bool FAST = decltype(fast_tag)::value >= 1 && !MN8;
+        constexpr bool FULL = decltype(fast_tag)::value >= 2 && !MN8;  // κs a multiple of 4·NCG: no batch tail
         // HOIST (κs = 4·NCG: exactly one batch of 4 chunks per thread): the thread's 4 keys and
         // row bases live in registers, reloaded once per input block instead of every stage
         constexpr bool HOIST = decltype(fast_tag)::value == 6;
@@ -1231,7 +1239,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
             }
             bool clear = local_no >= K::LOCALB;
             ++local_no;
-            const bool zero_fill = AFF ? kap_l > 4u * K::NCG : (DENSE ? false : (zf && p.C > 1u));
+            const bool zero_fill = AFF ? kap_l > 4u * K::NCG : ((DENSE || MN8) ? false : (zf && p.C > 1u));
             if (zero_fill && clear) {
               // more stale entries per thread than the 4 prev words hold: zero-fill the stage
               // cooperatively, then write (one barrier per stage)
@@ -1245,6 +1253,35 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
             for (int w = 0; w < NPW; ++w) nw[w] = 0;
             if (BPS_DBG(1)) {
               // experiment: no band generation (every generator variant)
+            } else if constexpr (MN8) {
+              // MN-major SW128 band tile: 64-row atoms 8 KB apart, input row u at u·128, the 16-byte
+              // piece of rows [ρ0, ρ0+8) at ((ρ0/8 ⊕ u) mod 8)·16.  One hash → the chunk's row offset
+              // (R3 with C = 8: z_hi >> 29) and sign → one one-hot piece, one conflict-free store
+              const uint32_t x = (uint32_t)uk;  // counter low word: (kc·64 + u) << 8
+              const uint32_t urow = sbase + u * 128u;
+              for (uint32_t t = 0; t < T; t += 4) {
+                uint32_t hi[4], lo[4], cr[4];
+  #pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const uint32_t c = (t + i < T) ? cg + K::NCG * (t + (uint32_t)i) : cg;
+                  const uint64_t k = ck[c];
+                  cr[i] = crow[c];
+                  mix64_folded((uint32_t)k, (uint32_t)(k >> 32), x, hi[i], lo[i]);
+                }
+  #pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  if (t + (uint32_t)i < T) {
+                    const uint32_t off = hi[i] >> 29;
+                    const uint32_t val = (0x3F80u | ((lo[i] & 1u) << 15)) << ((off & 1u) << 4);  // ±1.0 bf16
+                    const uint32_t ws = off >> 1;
+                    const uint32_t rho = cr[i];
+                    const uint32_t addr = urow + ((rho >> 6) << 13) + ((((rho >> 3) ^ u) & 7u) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(ws == 0u ? val : 0u),
+                                 "r"(ws == 1u ? val : 0u), "r"(ws == 2u ? val : 0u), "r"(ws == 3u ? val : 0u)
+                                 : "memory");
+                  }
+                }
+              }
             } else if constexpr (DENSE) {
               // C = B_r/s ∈ {1, 2, 4}: chunk c owns the CP band rows crow[c] .. +CP-1 and has exactly
               // one ±1 per column among them, so every row of the chunk is rewritten each stage as
@@ -1410,6 +1447,8 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
         band_gen(std::false_type{}, std::integral_constant<int, 4>{});
       else if (p.C == 4u)
         band_gen(std::false_type{}, std::integral_constant<int, 5>{});
+      else if (args.band_mn)
+        band_gen(std::false_type{}, std::integral_constant<int, 7>{});
       else if ((p.C & (p.C - 1u)) == 0u && ncomb == 4u * K::NCG && !args.nohoist)
         band_gen(std::false_type{}, std::integral_constant<int, 6>{});
       else if ((p.C & (p.C - 1u)) == 0u && ncomb % (4u * K::NCG) == 0u)
@@ -1794,6 +1833,9 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
     a.kgroup = 2;
   }
   a.nohoist = getenv("BPS_TC_NOHOIST") ? 1 : 0;
+  // BPS_TC_BANDMN=1 (experiment): MN-major one-hot band pieces for C = 8 row-partitioned sketches —
+  // parity-green, measured slower (smalln 1194 vs 1379, LS 5474 vs 5910, grad 5897 vs 6115 GB/s)
+  a.band_mn = (p.mode == 0 && p.C == 8u && p.B_r % 8 == 0 && getenv("BPS_TC_BANDMN")) ? 1 : 0;
   a.ab = getenv("BPS_TC_AB") ? atoi(getenv("BPS_TC_AB")) : 0;
   a.mma_hint = getenv("BPS_TC_MMA_HINT") ? (uint32_t)atoi(getenv("BPS_TC_MMA_HINT")) : 0u;  // A/B knob
   a.sleep_ns = getenv("BPS_TC_SLEEP") ? (uint32_t)atoi(getenv("BPS_TC_SLEEP")) : 20u;  // A/B knob
