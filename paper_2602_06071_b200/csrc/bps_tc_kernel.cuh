@@ -112,7 +112,7 @@ struct Cfg {
 #endif
   static constexpr int NBAND_CL = NMT == 1 ? BPS_NBAND_CLUSTER : (NMT == 2 ? 4 : 2);  // NMT = 4: 64 KB stages
 #ifndef BPS_NBAND_NARROW
-#define BPS_NBAND_NARROW 3
+#define BPS_NBAND_NARROW 2  // narrow tiles at two CTAs per SM: 2 buffers measured fastest (smalln 1645 vs 1378 with 3)
 #endif
   static constexpr int MINB = narrow_minb(F32, TRANS, NMT, BN_, CS, SS);  // CTAs per SM (bps_tc.h)
   static constexpr int NBAND = CS > 1 ? (NBAND_CL < CS ? CS : NBAND_CL)
@@ -122,7 +122,10 @@ struct Cfg {
   static constexpr int NRAW_FIT = (BUDGET - NBAND * BAND_STAGE) / RAW_STAGE;
   // ring depth: 8 stages, 16 for the narrow tile (BN = 64, small n: 8 KB stages, so that enough
   // bytes are in flight)
-  static constexpr int NRAW_MAX = BN_ <= 32 && !F32 ? (MINB >= 3 ? 8 : (MINB == 2 ? 12 : 24))
+#ifndef BPS_NARROW_NRAW32
+#define BPS_NARROW_NRAW32 12
+#endif
+  static constexpr int NRAW_MAX = BN_ <= 32 && !F32 ? (MINB >= 3 ? 8 : (MINB == 2 ? BPS_NARROW_NRAW32 : 24))
                                                    : (BN_ <= 64 && !F32 ? (MINB == 2 ? 8 : 16) : 8);
   static constexpr int NRAW = (NRAW_FIT > NRAW_MAX ? NRAW_MAX : NRAW_FIT) & (RL ? ~1 : ~0);  // RL: slot pairs
   static constexpr int OFF_RAW = 0;
@@ -1828,7 +1831,7 @@ int launch_impl(const SketchParams& p, const void* A, int64_t lda, int64_t n, fl
   // pairs never straddle an accumulation group, block or range (G, nk even; ranges start at groups)
   a.kstep = 1;
   if (!F32 && !TRANS && BN == 64 && CS == 1 && SS == 1 && NMT == 1 && K::NBAND % 2 == 0 && K::NRAW % 2 == 0 &&
-      hp.G % 2 == 0 && nk % 2 == 0 && !getenv("BPS_TC_KSTEP1")) {
+      hp.G % 2 == 0 && nk % 2 == 0 && getenv("BPS_TC_KSTEP2")) {  // opt-in: measured slower (n = 64: 2895 vs 3229 GB/s)
     a.kstep = 2;
     a.kgroup = 2;
   }
