@@ -57,6 +57,9 @@ namespace {
 #ifndef BPS_WARP_ARRIVE
 #define BPS_WARP_ARRIVE 1
 #endif
+#ifndef BPS_HOIST_FLAT
+#define BPS_HOIST_FLAT 1  // HOIST band generator with flat stale-entry offsets (A/B: -DBPS_HOIST_FLAT=0)
+#endif
 constexpr int kBandTile = 128 * kBK * 2;  // one M-tile (128 band rows) of a band stage, bytes
 constexpr int kMaxRanges = 511;           // canon: stream ranges per column tile (TcArgs::rb)
 constexpr int kMaxPeers = 8;              // output broadcast destinations (TcArgs::peer)
@@ -1176,7 +1179,17 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
   #pragma unroll
           for (int w = 0; w < NPW; ++w) prev[b][w] = 0;
         const uint32_t cshift = 32u - (31u - (uint32_t)__clz(p.C));  // FAST: off = z_hi >> (32 - log2 C)
-        if constexpr (FAST) {
+        if constexpr (HOIST && BPS_HOIST_FLAT) {
+          // HOIST: stale entries as full byte offsets, one per chunk (words 0-3); initially the first
+          // entry of the thread's own chunk (harmless to clear: zero, or rewritten right after)
+  #pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const uint32_t c = cg + K::NCG * w;
+            const uint32_t r = c < ncombo ? band_crow(p, c / p.s, c % p.s) : 0u;
+  #pragma unroll
+            for (int b = 0; b < K::LOCALB; ++b) prev[b][w] = r * 128u + (((r ^ ucol) & 7u) << 4);
+          }
+        } else if constexpr (FAST) {
           // before the first write of a buffer, "clear" the first entry of the thread's own chunk
           // (zero in a fresh buffer, and rewritten or left zero by the write that follows)
   #pragma unroll
@@ -1229,7 +1242,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
               ptx::named_bar_sync(1, K::NBANDT);
               if constexpr (HOIST) {
   #pragma unroll
-                for (int i = 0; i < 4; ++i) hk[i] = ck[cg + K::NCG * i], hc[i] = crow[cg + K::NCG * i];
+                for (int i = 0; i < 4; ++i) hk[i] = ck[cg + K::NCG * i], hc[i] = crow[cg + K::NCG * i] * 128u;
               }
               tr.add(7, t0);
             }
@@ -1318,6 +1331,24 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
                                : "memory");
                 }
               }
+            } else if constexpr (HOIST && BPS_HOIST_FLAT) {
+              // 4 chunks, keys and row-base byte offsets hc[i] = crow·128 in registers.  C ≥ 8 is a power
+              // of two, so chunk row bases are multiples of 8 and the SW128 16-byte index of row
+              // crow + r is (r ⊕ u/8) mod 8: one shift, one LOP3, one IMAD and one add per entry; the
+              // stale entry is a full byte offset (no unpacking)
+              const uint32_t x = (uint32_t)uk;  // counter low word: (kc·64 + u) << 8
+              const uint32_t ebase = sbase + ulo;
+              uint32_t hi[4], lo[4];
+  #pragma unroll
+              for (int i = 0; i < 4; ++i) mix64_folded((uint32_t)hk[i], (uint32_t)(hk[i] >> 32), x, hi[i], lo[i]);
+  #pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const uint32_t r = ptx::shr_clamp(hi[i], cshift);  // R3 for C = 2^m
+                const uint32_t off = hc[i] + r * 128u + (((r ^ ucol) & 7u) << 4);
+                ptx::st_shared_u16(ebase + prev[0][i], 0);
+                nw[i] = off;
+                ptx::st_shared_u16(ebase + off, (uint16_t)(0x3F80u | (lo[i] << 15)));  // ±1.0, sign = z & 1
+              }
             } else if constexpr (FAST) {
               const uint32_t x = (uint32_t)uk;  // counter low word: (kc·64 + u) << 8
               const uint32_t ebase = sbase + ulo;
@@ -1332,7 +1363,7 @@ __global__ void __launch_bounds__(Cfg<F32, TRANS, NMT, BN_, CS, TF, RL, SS>::NTH
   #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                   const uint64_t k = HOIST ? hk[i] : ckt[K::NCG * (4 * w + i)];
-                  cr[i] = HOIST ? hc[i] : crt[K::NCG * (4 * w + i)];
+                  cr[i] = HOIST ? hc[i] / 128u : crt[K::NCG * (4 * w + i)];
                   mix64_folded((uint32_t)k, (uint32_t)(k >> 32), x, hi[i], lo[i]);
                 }
   #pragma unroll
